@@ -1,0 +1,225 @@
+"""ORACLE (test infrastructure only) — all-at-once Uzawa V_var multigrid.
+
+Written from PAPER.md §5 with assembled scipy matrices:
+
+* Uzawa smoothing step, eq. (Uzawa_smooth)
+      u <- u + A^^-1 (f - A u - B^T p)
+      p <- p + S^^-1 (B u - C p - g)
+  A^ : symmetric coloured Gauss-Seidel on A ("symmetric hybrid parallel variant of
+       a row-wise red-black colored Gauss-Seidel").  Reading R12
+       (DESIGN.md): colours c(v) = (i+j+k) mod nc, colour passes 0..nc-1 then
+       nc-1..0; inside one colour pass every row of that colour is relaxed from
+       the vector at the start of the pass (Jacobi within a colour — the
+       "hybrid").  For rows without same-colour couplings this is exact GS.
+  S^ : "forward variant of the Gauss-Seidel method applied to ... C, with
+       omega = 0.3".  Reading R11: delta = one forward red-black GS sweep
+       on C delta = r from delta = 0, then p += omega * delta.
+* V_var cycle: nu_l = nu + nu_inc * l smoothing steps before and after
+  on level l (l = 0 finest; reading R13).
+* "Standard restriction and prolongation": P = coarse P1 basis evaluated
+  at fine vertices (plain definition of the nodal interpolation), R = P^T.
+* Coarse operators rediscretised per level (h_l = 1/n_l); coarse viscosity class
+  of a coarse tet = majority class of the fine tets it contains (ties -> larger mu,
+  then smaller class id).  Reading R15.
+* Coarsest level: exact solve ("a direct coarse grid solver ... is not
+  problematic") of the free-DoF system; without a traction face the pressure
+  constant is fixed by the Lagrange row w^T p = 0 (reading R9/R16).
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+from .fem import Problem, barycentric_gradients, kuhn_vertices
+from synth import PERMS
+
+
+def vertex_coords(n: int):
+    idx = np.arange(n + 1)
+    k, j, i = np.meshgrid(idx, idx, idx, indexing="ij")
+    return i.reshape(-1), j.reshape(-1), k.reshape(-1)
+
+
+def _locate(points: np.ndarray, nc: int, strict: bool):
+    """For points in coarse-grid units, the coarse (cube, type, barycentric) containing
+    them: barycentric coordinates w.r.t. each of the 6 Kuhn tets of the cube, first
+    tet with all coordinates >= 0 (strict: > 0)."""
+    cube = np.minimum(np.floor(points).astype(np.int64), nc - 1)
+    local = points - cube
+    found_t = np.full(len(points), -1)
+    lam_out = np.zeros((len(points), 4))
+    for t in range(6):
+        _, g = barycentric_gradients(kuhn_vertices(t))
+        a0 = kuhn_vertices(t)[0]
+        # lambda_i(q) = lambda_i(a0) + g_i . (q - a0);  lambda_i(a0) = delta_i0
+        lam = (local - a0) @ g.T
+        lam[:, 0] += 1.0
+        ok = (lam > 1e-12).all(axis=1) if strict else (lam > -1e-12).all(axis=1)
+        take = ok & (found_t < 0)
+        found_t[take] = t
+        lam_out[take] = lam[take]
+    assert (found_t >= 0).all()
+    return cube, found_t, lam_out
+
+
+def prolongation(nc: int) -> sp.csr_matrix:
+    """P[f, c] = phi_c(x_f): coarse P1 hat functions at the fine vertices (nf = 2 nc)."""
+    nf = 2 * nc
+    i, j, k = vertex_coords(nf)
+    pts = np.stack([i, j, k], axis=1) / 2.0
+    cube, t, lam = _locate(pts, nc, strict=False)
+    rows, cols, vals = [], [], []
+    N1 = nc + 1
+    for m in range(4):
+        off = np.stack([kuhn_vertices(tt)[m] for tt in range(6)]).astype(np.int64)[t]
+        cv = cube + off
+        cid = cv[:, 0] + N1 * (cv[:, 1] + N1 * cv[:, 2])
+        keep = np.abs(lam[:, m]) > 1e-14
+        rows.append(np.arange(len(pts))[keep])
+        cols.append(cid[keep])
+        vals.append(lam[keep, m])
+    P = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=((nf + 1) ** 3, N1 ** 3))
+    P.sum_duplicates()
+    return P
+
+
+def coarse_classes(nf: int, cls_f: np.ndarray, class_mu) -> np.ndarray:
+    """Coarse element classes: majority vote over the 8 fine tets inside each coarse
+    tet (fine tet assigned to the coarse tet containing its centroid)."""
+    nc = nf // 2
+    class_mu = np.asarray(class_mu, dtype=np.float64)
+    K = len(class_mu)
+    cls_f = np.asarray(cls_f).reshape(nf, nf, nf, 6)
+    counts = np.zeros((nc, nc, nc, 6, K), dtype=np.int64)
+    idx = np.arange(nf)
+    kk, jj, ii = np.meshgrid(idx, idx, idx, indexing="ij")
+    for t in range(6):
+        cen = kuhn_vertices(t).mean(axis=0)
+        pts = np.stack([ii.reshape(-1) + cen[0], jj.reshape(-1) + cen[1],
+                        kk.reshape(-1) + cen[2]], axis=1) / 2.0
+        cube, tc, _ = _locate(pts, nc, strict=True)
+        c = cls_f[..., t].reshape(-1)
+        np.add.at(counts, (cube[:, 2], cube[:, 1], cube[:, 0], tc, c), 1)
+    assert (counts.sum(axis=-1) == 8).all()
+    # majority; ties -> larger mu, then smaller class id
+    order = sorted(range(K), key=lambda q: (-class_mu[q], q))
+    best = np.full(counts.shape[:-1], order[0])
+    bestc = counts[..., order[0]]
+    for q in order[1:]:
+        better = counts[..., q] > bestc
+        best = np.where(better, q, best)
+        bestc = np.where(better, counts[..., q], bestc)
+    return best.astype(np.uint8).reshape(-1)
+
+
+class Level:
+    def __init__(self, n, cls, class_mu, faces, form, delta):
+        self.n = n
+        self.cls = np.asarray(cls, dtype=np.uint8)
+        self.prob = Problem(n, np.asarray(class_mu)[self.cls], faces, form, delta)
+        i, j, k = vertex_coords(n)
+        self.parity = (i + j + k)
+        V = self.prob.V
+        self.diagA = self.prob.A.diagonal()
+        self.diagC = self.prob.C.diagonal()
+        self.free_u = self.prob.free[:3 * V]
+
+
+class Hierarchy:
+    def __init__(self, n, cls, class_mu, faces, form="mod", delta=1.0 / 12.0,
+                 n_coarse=4, nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2):
+        self.levels = []
+        self.P = []
+        c = np.asarray(cls, dtype=np.uint8)
+        m = n
+        while True:
+            self.levels.append(Level(m, c, class_mu, faces, form, delta))
+            if m <= n_coarse:
+                break
+            assert m % 2 == 0
+            self.P.append(prolongation(m // 2))
+            c = coarse_classes(m, c, class_mu)
+            m //= 2
+        self.nu_pre, self.nu_post, self.nu_inc = nu_pre, nu_post, nu_inc
+        self.omega = omega
+        self.ncolors_u = ncolors_u
+        self._coarse_setup()
+
+    # -- smoother ----------------------------------------------------------
+    def uzawa(self, lev: Level, x: np.ndarray, b: np.ndarray) -> np.ndarray:
+        pr = lev.prob
+        V = pr.V
+        x = x.copy()
+        u, p = x[:3 * V], x[3 * V:]
+        f, g = b[:3 * V], b[3 * V:]
+        rhs = f - pr.B.T @ p
+        nc = self.ncolors_u
+        col_u = np.tile(lev.parity % nc, 3)
+        for c in list(range(nc)) + list(reversed(range(nc))):
+            r = rhs - pr.A @ u
+            sel = (col_u == c) & lev.free_u
+            u[sel] += r[sel] / lev.diagA[sel]
+        rp = pr.B @ u - pr.C @ p - g
+        d = np.zeros(V)
+        col_p = lev.parity % 2
+        for c in range(2):
+            s = rp - pr.C @ d
+            sel = col_p == c
+            d[sel] += s[sel] / lev.diagC[sel]
+        p += self.omega * d
+        return x
+
+    # -- coarse solve ------------------------------------------------------
+    def _coarse_setup(self):
+        lev = self.levels[-1]
+        pr = lev.prob
+        free = np.flatnonzero(pr.free)
+        Kff = pr.K[free][:, free].toarray()
+        if not pr.has_traction:
+            w = np.concatenate([np.zeros(3 * pr.V), pr.gauge_w])[free]
+            N = len(free)
+            Kaug = np.zeros((N + 1, N + 1))
+            Kaug[:N, :N] = Kff
+            Kaug[:N, N] = w
+            Kaug[N, :N] = w
+            self.G = np.linalg.inv(Kaug)[:N, :N]
+        else:
+            self.G = np.linalg.inv(Kff)
+        self.coarse_free = free
+
+    def coarse_solve(self, b):
+        x = np.zeros_like(b)
+        x[self.coarse_free] = self.G @ b[self.coarse_free]
+        return x
+
+    # -- cycle -------------------------------------------------------------
+    def vcycle(self, b, x, l=0):
+        lev = self.levels[l]
+        if l == len(self.levels) - 1:
+            return self.coarse_solve(b)
+        for _ in range(self.nu_pre + self.nu_inc * l):
+            x = self.uzawa(lev, x, b)
+        r = b - lev.prob.apply(x)
+        P = self.P[l]
+        Vc = self.levels[l + 1].prob.V
+        bc = np.concatenate([P.T @ r.reshape(4, -1)[f] for f in range(4)])
+        bc = np.where(self.levels[l + 1].prob.free, bc, 0.0)
+        xc = self.vcycle(bc, np.zeros(4 * Vc), l + 1)
+        x = x + np.concatenate([P @ xc.reshape(4, -1)[f] for f in range(4)])
+        x = np.where(lev.prob.free, x, 0.0)
+        for _ in range(self.nu_post + self.nu_inc * l):
+            x = self.uzawa(lev, x, b)
+        return x
+
+    def solve(self, b, rtol=1e-8, max_cycles=100, x0=None):
+        top = self.levels[0].prob
+        x = np.zeros_like(b) if x0 is None else x0.copy()
+        nb = np.linalg.norm(b)
+        hist = [np.linalg.norm(b - top.apply(x)) / nb]
+        for _ in range(max_cycles):
+            x = self.vcycle(b, x)
+            hist.append(np.linalg.norm(b - top.apply(x)) / nb)
+            if hist[-1] <= rtol:
+                break
+        return top.gauge(x), hist
