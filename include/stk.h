@@ -1,0 +1,180 @@
+/*
+ * stk.h — C ABI of the B200-native matrix-free Stokes operator and Uzawa
+ * multigrid (data-parallel hot path of arXiv:1604.07994, "A symmetric decoupled
+ * weak formulation ..." — citations P:L are PAPER.md line numbers).
+ *
+ * Problem: on the unit cube, uniformly refined into
+ * n^3 cubes x 6 Kuhn tetrahedra, with element-wise constant viscosity
+ * mu_T, find P1 velocity u and P1 pressure p with
+ *
+ *     [ A   B^T ] [u]   [f_h]        A : modified viscous form a_tr
+ *     [ B   -C  ] [p] = [ g ]        B : b(v,q) = -(div v, q)
+ *                                    C : pressure stabilisation (DESIGN R1)
+ *
+ * A is applied matrix-free: per-class constant Laplacian stencils inside the
+ * isoviscous subdomains, full a_tr rows only at the interface Gamma_12 and
+ * the traction boundary Gamma_F (eq. equivalence-stencil).
+ *
+ * Conventions (all calls):
+ *  - Every call returns stk_status; no C++ exception crosses the ABI.
+ *  - "dev" pointers are CUDA device pointers (e.g. torch tensors' data_ptr);
+ *    "host" pointers are CPU memory.  The caller owns every pointer it passes;
+ *    setup arrays are copied during the call.  The context owns the level
+ *    hierarchy, stencils, interface data, coarse inverse and communicator.
+ *  - Device vectors hold 4 fields (u1,u2,u3,p) in the padded z-slab layout
+ *    returned by stk_layout (element (f,i,j,k) at
+ *    f*field_stride + (k - z0 + 1)*pitch_y + j*pitch_x + i, doubles; planes
+ *    k = z0-1 and z0+nz_local are halo planes owned by the neighbours).
+ *    Allocate stk_layout(...).vec_len doubles per vector.
+ *  - Velocity entries at Dirichlet vertices (closure of Dirichlet faces) are
+ *    ignored on input (treated as 0) and written as 0 on output.  Pressure
+ *    lives at every vertex.
+ *  - All device work is stream-ordered on cfg.stream; calls return before the
+ *    work completes, except stk_solve and calls that return host data.
+ *  - Errors: STK_EINVAL bad argument / size; STK_ESTATE call order violated
+ *    (create -> set_viscosity -> assemble -> the rest); STK_ECUDA / STK_ENCCL
+ *    a CUDA / NCCL failure (message in stk_last_error); STK_ENOCONV the solve
+ *    did not reach rtol (the iterate and history are still written).
+ */
+#ifndef STK_H
+#define STK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct stk_ctx stk_ctx;
+
+typedef enum {
+  STK_OK = 0,
+  STK_ENOCONV = 1,
+  STK_EINVAL = -1,
+  STK_ENOMEM = -2,
+  STK_ECUDA = -3,
+  STK_ENCCL = -4,
+  STK_ESTATE = -5,
+  STK_EUNSUP = -6
+} stk_status;
+
+/* viscous form of the A block: modified a_tr, strain a_sym,
+ * gradient (mu grad u, grad v) */
+typedef enum { STK_FORM_MOD = 0, STK_FORM_SYM = 1, STK_FORM_GRAD = 2 } stk_form;
+/* faces x0,x1,y0,y1,z0,z1: homogeneous Dirichlet u = 0 or traction
+ * free sigma n = 0; Dirichlet wins on shared edges/corners */
+typedef enum { STK_FACE_DIRICHLET0 = 0, STK_FACE_TRACTION = 1 } stk_face;
+/* block mask for stk_apply: y_u = [A u] + [B^T p], y_p = [B u] - [C p] */
+enum { STK_BLK_A = 1, STK_BLK_BT = 2, STK_BLK_B = 4, STK_BLK_C = 8, STK_BLK_ALL = 15 };
+/* where a canonical (non-padded) array lives */
+enum { STK_HOST = 0, STK_DEVICE = 1 };
+
+typedef struct {
+  int32_t n;          /* finest intervals per direction, power of 2, >= 4 */
+  int32_t n_coarse;   /* coarsest level intervals (direct solve), default 4 */
+  int32_t form;       /* stk_form */
+  int32_t face[6];    /* stk_face per face */
+  double delta;       /* stabilisation constant, c(p,q) = sum_T delta h^2/mu_T (grad p, grad q)_T; default 1/12 */
+  int32_t nu_pre, nu_post, nu_inc; /* V_var smoothing: nu + nu_inc * level (DESIGN R13) */
+  double omega;       /* Schur-complement under-relaxation, 0.3 */
+  int32_t ncolors_u;  /* velocity GS colours (i+j+k) mod ncolors_u: 2 (red-black) or 4 */
+  int32_t rank, nranks; /* z-slab owner and number of ranks (one GPU each) */
+  void* stream;       /* cudaStream_t; NULL = legacy default stream */
+} stk_config;
+
+typedef struct {
+  int32_t n;          /* intervals of this level */
+  int32_t nx, ny;     /* n+1 vertices in x and y */
+  int32_t nz_local;   /* vertex planes owned by this rank */
+  int32_t z0;         /* global index of the first owned plane */
+  int64_t pitch_x, pitch_y, field_stride; /* in doubles */
+  int64_t vec_len;    /* doubles per 4-field vector */
+  int64_t n_irregular; /* vertices whose rows use the full (interface/boundary) stencil */
+  int64_t n_vertices; /* owned vertices */
+} stk_layout_t;
+
+typedef struct {
+  int32_t cycles;
+  double rho;         /* mean residual reduction factor of the last cycles */
+  double rel_res;     /* ||b - K x|| / ||b|| over free DoFs */
+  double t_total_s;   /* device time of the solve */
+  double res_hist[256];
+  int32_t nan_seen;
+} stk_report;
+
+/* NCCL unique id for nranks > 1: call on rank 0, broadcast the 128 bytes
+ * (e.g. with torch.distributed), pass to stk_create on every rank. */
+stk_status stk_nccl_unique_id(uint8_t id[128]);
+
+/* Create a context on the current CUDA device.  Checks n (power of 2,
+ * n/nranks divisible by 2 on every distributed level).  id may be NULL when
+ * nranks == 1. */
+stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out);
+
+/* Element viscosity partition.  elem_class: host uint8 array of this
+ * rank's cube layers cz in [z0_cubes, z1_cubes) (see stk_cube_range), layout
+ * [cz][cj][ci][t], t = Kuhn permutation index; class_mu: nclass
+ * (<= 255) viscosities > 0.  Both copied. */
+stk_status stk_set_viscosity(stk_ctx* ctx, const uint8_t* elem_class, const double* class_mu,
+                             int32_t nclass);
+/* cube layers [*z0, *z1) this rank must pass to stk_set_viscosity */
+stk_status stk_cube_range(const stk_ctx* ctx, int32_t* z0, int32_t* z1);
+
+/* Assemble all levels: coarse viscosity classes (majority of the 8 Bey children),
+ * per-vertex classification (regular class k / interface-or-boundary row),
+ * constant subdomain stencils per class, and the coarsest-level inverse. */
+stk_status stk_assemble(stk_ctx* ctx);
+
+stk_status stk_layout(const stk_ctx* ctx, int32_t level, stk_layout_t* out);
+
+/* canonical <-> padded device layout.  canon: 4 fields x (n+1)^3 doubles,
+ * field-major, vertex v = i + (n+1)(j + (n+1)k) (this rank's owned planes only:
+ * 4 x (n+1)^2 x nz_local, planes z0..z0+nz_local-1).  where = STK_HOST/DEVICE. */
+stk_status stk_import(stk_ctx* ctx, int32_t level, const double* canon, int32_t where,
+                      double* dev_vec);
+stk_status stk_export(stk_ctx* ctx, int32_t level, const double* dev_vec, double* canon,
+                      int32_t where);
+
+/* Right-hand side b = (f_h, 0).  kind 0: nodal f (canonical
+ * 3 x (n+1)^2 x nz_local device array), b_u = consistent mass * f.
+ * kind 1: element-constant f: f_dev = uint8 forcing class per element (same
+ * layout as stk_set_viscosity), table = host 3 x nftab doubles. */
+stk_status stk_load_vector(stk_ctx* ctx, int32_t kind, const void* f_dev, const double* table,
+                           int32_t nftab, double* b_dev);
+
+/* y = K x restricted to the requested blocks (STK_BLK_*) on level `level`
+ * (0 = finest).  The measured hot kernel. */
+stk_status stk_apply(stk_ctx* ctx, int32_t level, uint32_t blocks, const double* x, double* y);
+/* r = b - K x; if norms != NULL, writes host norms[5] = ||r_u1||^2, ||r_u2||^2,
+ * ||r_u3||^2, ||r_p||^2, total (all ranks; synchronises). */
+stk_status stk_residual(stk_ctx* ctx, int32_t level, const double* x, const double* b, double* r,
+                        double* norms);
+/* `steps` Uzawa smoothing steps in place on x. */
+stk_status stk_smooth(stk_ctx* ctx, int32_t level, double* x, const double* b, int32_t steps);
+/* b_c = R r_f = P^T r_f, coarse level = fine_level + 1 */
+stk_status stk_restrict(stk_ctx* ctx, int32_t fine_level, const double* r_f, double* b_c);
+/* x_f += P x_c (linear interpolation on coarse Kuhn edges) */
+stk_status stk_prolong_add(stk_ctx* ctx, int32_t coarse_level, const double* x_c, double* x_f);
+/* one V_var cycle on the finest level, in place on x */
+stk_status stk_vcycle(stk_ctx* ctx, const double* b, double* x);
+/* V-cycles until ||b-Kx||/||b|| <= rtol (synchronous); gauge applied at the end */
+stk_status stk_solve(stk_ctx* ctx, const double* b, double* x, double rtol, int32_t max_cycles,
+                     stk_report* report);
+/* subtract the mu^-1-weighted mean pressure (Q of P:136); no-op with traction faces */
+stk_status stk_gauge(stk_ctx* ctx, int32_t level, double* x);
+/* per-field squared norms of a level vector over owned free DoFs (host out[5]) */
+stk_status stk_norms(stk_ctx* ctx, int32_t level, const double* x, double* out);
+
+/* Optional: select the kernel implementation for levels >= 64 intervals:
+ * 1 = tiled constant-stencil kernels (default), 0 = generic element-row kernels. */
+stk_status stk_set_kernel_mode(stk_ctx* ctx, int32_t mode);
+/* Number of kernels this context launched so far (evidence counter). */
+int64_t stk_launch_count(const stk_ctx* ctx);
+
+const char* stk_last_error(const stk_ctx* ctx);
+stk_status stk_destroy(stk_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STK_H */

@@ -1,0 +1,295 @@
+"""B200-native matrix-free Stokes operator and Uzawa multigrid (arXiv:1604.07994).
+
+Thin Python binding of the C ABI in ``include/stk.h`` (``libstk.so``, built
+in-tree by ``paper_1604_07994_b200.build``).  Argument marshalling only: every
+step of the operator and solver runs in the library's CUDA kernels.  There is
+no CPU fallback — importing this package without the built library raises.
+
+Functions keep the C names (``stk_create``, ``stk_apply``, ...).  The
+``StokesContext`` class bundles them for torch device tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libstk.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python paper_1604_07994_b200/build.py` "
+        "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+STK_OK, STK_ENOCONV, STK_EINVAL, STK_ENOMEM, STK_ECUDA, STK_ENCCL, STK_ESTATE, STK_EUNSUP = (
+    0, 1, -1, -2, -3, -4, -5, -6)
+FORMS = {"mod": 0, "sym": 1, "grad": 2}
+BLK_A, BLK_BT, BLK_B, BLK_C, BLK_ALL = 1, 2, 4, 8, 15
+HOST, DEVICE = 0, 1
+
+
+class stk_config(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("n_coarse", ctypes.c_int32), ("form", ctypes.c_int32),
+                ("face", ctypes.c_int32 * 6), ("delta", ctypes.c_double),
+                ("nu_pre", ctypes.c_int32), ("nu_post", ctypes.c_int32), ("nu_inc", ctypes.c_int32),
+                ("omega", ctypes.c_double), ("ncolors_u", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("stream", ctypes.c_void_p)]
+
+
+class stk_layout_t(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("nx", ctypes.c_int32), ("ny", ctypes.c_int32),
+                ("nz_local", ctypes.c_int32), ("z0", ctypes.c_int32),
+                ("pitch_x", ctypes.c_int64), ("pitch_y", ctypes.c_int64),
+                ("field_stride", ctypes.c_int64), ("vec_len", ctypes.c_int64),
+                ("n_irregular", ctypes.c_int64), ("n_vertices", ctypes.c_int64)]
+
+
+class stk_report(ctypes.Structure):
+    _fields_ = [("cycles", ctypes.c_int32), ("rho", ctypes.c_double), ("rel_res", ctypes.c_double),
+                ("t_total_s", ctypes.c_double), ("res_hist", ctypes.c_double * 256),
+                ("nan_seen", ctypes.c_int32)]
+
+
+_P = ctypes.c_void_p
+_S = ctypes.c_int
+_sigs = {
+    "stk_nccl_unique_id": [_P],
+    "stk_create": [ctypes.POINTER(stk_config), _P, ctypes.POINTER(_P)],
+    "stk_set_viscosity": [_P, _P, _P, ctypes.c_int32],
+    "stk_cube_range": [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
+    "stk_assemble": [_P],
+    "stk_layout": [_P, ctypes.c_int32, ctypes.POINTER(stk_layout_t)],
+    "stk_import": [_P, ctypes.c_int32, _P, ctypes.c_int32, _P],
+    "stk_export": [_P, ctypes.c_int32, _P, _P, ctypes.c_int32],
+    "stk_load_vector": [_P, ctypes.c_int32, _P, _P, ctypes.c_int32, _P],
+    "stk_apply": [_P, ctypes.c_int32, ctypes.c_uint32, _P, _P],
+    "stk_residual": [_P, ctypes.c_int32, _P, _P, _P, _P],
+    "stk_smooth": [_P, ctypes.c_int32, _P, _P, ctypes.c_int32],
+    "stk_restrict": [_P, ctypes.c_int32, _P, _P],
+    "stk_prolong_add": [_P, ctypes.c_int32, _P, _P],
+    "stk_vcycle": [_P, _P, _P],
+    "stk_solve": [_P, _P, _P, ctypes.c_double, ctypes.c_int32, ctypes.POINTER(stk_report)],
+    "stk_gauge": [_P, ctypes.c_int32, _P],
+    "stk_norms": [_P, ctypes.c_int32, _P, _P],
+    "stk_set_kernel_mode": [_P, ctypes.c_int32],
+    "stk_destroy": [_P],
+}
+for _name, _args in _sigs.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _S
+_lib.stk_last_error.argtypes = [_P]
+_lib.stk_last_error.restype = ctypes.c_char_p
+_lib.stk_launch_count.argtypes = [_P]
+_lib.stk_launch_count.restype = ctypes.c_int64
+
+# C names re-exported verbatim
+for _name in list(_sigs) + ["stk_last_error", "stk_launch_count"]:
+    globals()[_name] = getattr(_lib, _name)
+
+
+class StkError(RuntimeError):
+    def __init__(self, call, status, msg):
+        super().__init__(f"{call} failed with status {status}: {msg}")
+        self.status = status
+
+
+def _ptr(t):
+    """device/host pointer of a torch tensor or numpy array (no copies)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        assert t.flags["C_CONTIGUOUS"]
+        return t.ctypes.data
+    assert t.is_contiguous()
+    return t.data_ptr()
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    s = _lib.stk_nccl_unique_id(buf)
+    if s != STK_OK:
+        raise StkError("stk_nccl_unique_id", s, "NCCL unavailable")
+    return bytes(buf)
+
+
+class StokesContext:
+    """One rank (one GPU) of the distributed operator / solver."""
+
+    def __init__(self, n, form="mod", faces=(0,) * 6, delta=1.0 / 12.0, n_coarse=4,
+                 nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2, rank=0, nranks=1,
+                 stream=None, nccl_id: bytes | None = None):
+        import torch
+        self.torch = torch
+        cfg = stk_config()
+        cfg.n, cfg.n_coarse, cfg.form = n, n_coarse, FORMS[form]
+        for f in range(6):
+            cfg.face[f] = int(faces[f])
+        cfg.delta, cfg.nu_pre, cfg.nu_post, cfg.nu_inc = delta, nu_pre, nu_post, nu_inc
+        cfg.omega, cfg.ncolors_u, cfg.rank, cfg.nranks = omega, ncolors_u, rank, nranks
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        self.stream = stream
+        cfg.stream = stream.cuda_stream
+        self.cfg = cfg
+        self.n, self.form, self.faces = n, form, tuple(faces)
+        h = _P()
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+        s = _lib.stk_create(ctypes.byref(cfg), idbuf, ctypes.byref(h))
+        self.h = h
+        if s != STK_OK:
+            msg = _lib.stk_last_error(h).decode() if h.value else ""
+            if h.value:
+                _lib.stk_destroy(h)
+                self.h = None
+            raise StkError("stk_create", s, msg)
+        self.nlev = 0
+        while True:
+            lay = stk_layout_t()
+            if _lib.stk_layout(self.h, self.nlev, ctypes.byref(lay)) != STK_OK:
+                break
+            self.nlev += 1
+
+    # -- plumbing -------------------------------------------------------------
+    def _chk(self, call, s, allow=(STK_OK,)):
+        if s not in allow:
+            raise StkError(call, s, _lib.stk_last_error(self.h).decode())
+        return s
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.stk_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def layout(self, level=0) -> stk_layout_t:
+        lay = stk_layout_t()
+        self._chk("stk_layout", _lib.stk_layout(self.h, level, ctypes.byref(lay)))
+        return lay
+
+    def cube_range(self):
+        a, b = ctypes.c_int32(), ctypes.c_int32()
+        self._chk("stk_cube_range", _lib.stk_cube_range(self.h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def new_vector(self, level=0):
+        return self.torch.zeros(self.layout(level).vec_len, dtype=self.torch.float64, device="cuda")
+
+    # -- setup ----------------------------------------------------------------
+    def set_viscosity(self, elem_class: np.ndarray, class_mu):
+        ec = np.ascontiguousarray(elem_class, dtype=np.uint8)
+        mu = np.ascontiguousarray(class_mu, dtype=np.float64)
+        self._chk("stk_set_viscosity", _lib.stk_set_viscosity(self.h, _ptr(ec), _ptr(mu), len(mu)))
+
+    def assemble(self):
+        self._chk("stk_assemble", _lib.stk_assemble(self.h))
+
+    def set_kernel_mode(self, mode: int):
+        self._chk("stk_set_kernel_mode", _lib.stk_set_kernel_mode(self.h, mode))
+
+    def launch_count(self) -> int:
+        return _lib.stk_launch_count(self.h)
+
+    # -- vectors --------------------------------------------------------------
+    def import_(self, canon, level=0, out=None):
+        """canonical (4, owned vertices) host numpy or device tensor -> padded device vector."""
+        out = self.new_vector(level) if out is None else out
+        if isinstance(canon, np.ndarray):
+            c = np.ascontiguousarray(canon, dtype=np.float64)
+            self._chk("stk_import", _lib.stk_import(self.h, level, _ptr(c), HOST, _ptr(out)))
+        else:
+            c = canon.contiguous()
+            self._chk("stk_import", _lib.stk_import(self.h, level, _ptr(c), DEVICE, _ptr(out)))
+        return out
+
+    def export(self, vec, level=0) -> np.ndarray:
+        lay = self.layout(level)
+        out = np.empty((4, lay.n_vertices), dtype=np.float64)
+        self._chk("stk_export", _lib.stk_export(self.h, level, _ptr(vec), _ptr(out), HOST))
+        return out
+
+    def export_device(self, vec, level=0, out=None):
+        lay = self.layout(level)
+        out = self.torch.empty((4, lay.n_vertices), dtype=self.torch.float64, device="cuda") if out is None else out
+        self._chk("stk_export", _lib.stk_export(self.h, level, _ptr(vec), _ptr(out), DEVICE))
+        return out
+
+    def load_nodal(self, f_canon, b=None):
+        """b = (M f, 0) for nodal forcing f (3, owned vertices)."""
+        lay = self.layout(0)
+        f4 = np.zeros((4, lay.n_vertices)) if isinstance(f_canon, np.ndarray) else None
+        if f4 is not None:
+            f4[:3] = f_canon
+            fv = self.import_(f4)
+        else:
+            t = self.torch.zeros((4, lay.n_vertices), dtype=self.torch.float64, device="cuda")
+            t[:3] = f_canon
+            fv = self.import_(t)
+        b = self.new_vector(0) if b is None else b
+        self._chk("stk_load_vector", _lib.stk_load_vector(self.h, 0, _ptr(fv), None, 0, _ptr(b)))
+        return b
+
+    def load_element(self, f_cls: np.ndarray, table, b=None):
+        fc = self.torch.from_numpy(np.ascontiguousarray(f_cls, dtype=np.uint8)).cuda()
+        tab = np.ascontiguousarray(table, dtype=np.float64).reshape(-1)
+        b = self.new_vector(0) if b is None else b
+        self._chk("stk_load_vector", _lib.stk_load_vector(self.h, 1, _ptr(fc), _ptr(tab),
+                                                          len(tab) // 3, _ptr(b)))
+        self.torch.cuda.current_stream().synchronize()
+        return b
+
+    # -- operator / solver ------------------------------------------------------
+    def apply(self, x, y=None, level=0, blocks=BLK_ALL):
+        y = self.new_vector(level) if y is None else y
+        self._chk("stk_apply", _lib.stk_apply(self.h, level, blocks, _ptr(x), _ptr(y)))
+        return y
+
+    def residual(self, x, b, r=None, level=0, norms=False):
+        r = self.new_vector(level) if r is None else r
+        nb = np.zeros(5) if norms else None
+        self._chk("stk_residual", _lib.stk_residual(self.h, level, _ptr(x), _ptr(b), _ptr(r), _ptr(nb)))
+        return (r, nb) if norms else r
+
+    def norms(self, x, level=0):
+        out = np.zeros(5)
+        self._chk("stk_norms", _lib.stk_norms(self.h, level, _ptr(x), _ptr(out)))
+        return out
+
+    def smooth(self, x, b, steps=1, level=0):
+        self._chk("stk_smooth", _lib.stk_smooth(self.h, level, _ptr(x), _ptr(b), steps))
+        return x
+
+    def restrict(self, r_f, b_c=None, fine_level=0):
+        b_c = self.new_vector(fine_level + 1) if b_c is None else b_c
+        self._chk("stk_restrict", _lib.stk_restrict(self.h, fine_level, _ptr(r_f), _ptr(b_c)))
+        return b_c
+
+    def prolong_add(self, x_c, x_f, coarse_level=1):
+        self._chk("stk_prolong_add", _lib.stk_prolong_add(self.h, coarse_level, _ptr(x_c), _ptr(x_f)))
+        return x_f
+
+    def vcycle(self, b, x):
+        self._chk("stk_vcycle", _lib.stk_vcycle(self.h, _ptr(b), _ptr(x)))
+        return x
+
+    def gauge(self, x, level=0):
+        self._chk("stk_gauge", _lib.stk_gauge(self.h, level, _ptr(x)))
+        return x
+
+    def solve(self, b, x=None, rtol=1e-8, max_cycles=100, raise_on_noconv=False):
+        x = self.new_vector(0) if x is None else x
+        rep = stk_report()
+        s = _lib.stk_solve(self.h, _ptr(b), _ptr(x), rtol, max_cycles, ctypes.byref(rep))
+        self._chk("stk_solve", s, allow=(STK_OK,) if raise_on_noconv else (STK_OK, STK_ENOCONV))
+        return x, rep

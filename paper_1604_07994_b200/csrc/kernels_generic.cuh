@@ -1,0 +1,504 @@
+// Generic (element-row) kernels: one thread per owned vertex, every row by
+// the element loop of row_generic.  Used on the small levels (n < 64) and as
+// the reference device path for the tiled constant-stencil kernels.
+#pragma once
+#include "stk_common.cuh"
+
+namespace stk {
+
+__device__ __forceinline__ bool owned_vertex(const DGrid& g, int64_t t, int& i, int& j, int& k) {
+  const int64_t nx = g.n + 1;
+  const int64_t per = nx * nx;
+  if (t >= per * g.nzl) return false;
+  k = g.z0 + (int)(t / per);
+  const int64_t r = t % per;
+  j = (int)(r / nx);
+  i = (int)(r % nx);
+  return true;
+}
+
+template <int FORM>
+__global__ void k_apply_generic(DGrid g, const double* __restrict__ x, double* __restrict__ y,
+                                unsigned blocks) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  FetchVec fx{x, x + 3 * g.fs};
+  double r[4], dA[3], dC;
+  row_generic<FORM>(g, i, j, k, fx, blocks, r, dA, dC);
+  const int64_t o = vidx(g, i, j, k);
+#pragma unroll
+  for (int f = 0; f < 4; ++f) y[f * g.fs + o] = r[f];
+}
+
+// r = b - K x  (velocity rows 0 at Dirichlet vertices)
+template <int FORM>
+__global__ void k_residual_generic(DGrid g, const double* __restrict__ x,
+                                   const double* __restrict__ b, double* __restrict__ r) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  FetchVec fx{x, x + 3 * g.fs};
+  double y[4], dA[3], dC;
+  row_generic<FORM>(g, i, j, k, fx, BLK_ALL, y, dA, dC);
+  const int64_t o = vidx(g, i, j, k);
+  const bool dir = is_dirichlet(g, i, j, k);
+#pragma unroll
+  for (int f = 0; f < 4; ++f) r[f * g.fs + o] = (f < 3 && dir) ? 0.0 : b[f * g.fs + o] - y[f];
+}
+
+// One colour pass of the velocity Gauss-Seidel (Jacobi within the colour):
+//   u_out = u_in + (f - A u_in - B^T p) / diag(A)  at vertices of colour `color`
+//   u_out = u_in                                  elsewhere
+template <int FORM>
+__global__ void k_vel_pass_generic(DGrid g, const double* __restrict__ uin,
+                                   const double* __restrict__ p, const double* __restrict__ b,
+                                   double* __restrict__ uout, int color, int ncolors) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  const int64_t o = vidx(g, i, j, k);
+  const bool active = ((i + j + k) % ncolors == color) && !is_dirichlet(g, i, j, k);
+  if (!active) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) uout[a * g.fs + o] = is_dirichlet(g, i, j, k) ? 0.0 : uin[a * g.fs + o];
+    return;
+  }
+  FetchVec fx{uin, p};
+  double y[4], dA[3], dC;
+  row_generic<FORM>(g, i, j, k, fx, BLK_A | BLK_BT, y, dA, dC);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) uout[a * g.fs + o] = uin[a * g.fs + o] + (b[a * g.fs + o] - y[a]) / dA[a];
+}
+
+// Pressure step, part 1:  r_p = B u - C p - g ;  T = r_p / C_ii (colour 0), r_p (colour 1)
+template <int FORM>
+__global__ void k_p_pass1_generic(DGrid g, const double* __restrict__ x,
+                                  const double* __restrict__ gp, double* __restrict__ T) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  FetchVec fx{x, x + 3 * g.fs};
+  double y[4], dA[3], dC;
+  row_generic<FORM>(g, i, j, k, fx, BLK_B | BLK_C, y, dA, dC);
+  const int64_t o = vidx(g, i, j, k);
+  const double r = y[3] - gp[o];
+  T[o] = ((i + j + k) & 1) == 0 ? r / dC : r;
+}
+
+// masked fetch: pressure = T at colour-0 vertices, 0 elsewhere; velocity 0
+struct FetchRedP {
+  const double* __restrict__ T;
+  __device__ __forceinline__ double operator()(const DGrid& g, int i, int j, int k, int f) const {
+    if (f != 3 || ((i + j + k) & 1)) return 0.0;
+    return T[vidx(g, i, j, k)];
+  }
+};
+
+// Pressure step, part 2: delta_1 = (r_p - C delta_0)/C_ii on colour 1,
+// delta_0 = T on colour 0;  p += omega * delta
+template <int FORM>
+__global__ void k_p_pass2_generic(DGrid g, const double* __restrict__ T, double* __restrict__ p,
+                                  double omega) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  const int64_t o = vidx(g, i, j, k);
+  double d;
+  if (((i + j + k) & 1) == 0) {
+    d = T[o];
+  } else {
+    FetchRedP fx{T};
+    double y[4], dA[3], dC;
+    row_generic<FORM>(g, i, j, k, fx, BLK_C, y, dA, dC);
+    d = (T[o] + y[3]) / dC;   // y[3] = -(C delta_0)_i
+  }
+  p[o] += omega * d;
+}
+
+// b_c = P^T r_f: (R r)(I) = r(2I) + 1/2 sum_{d in +-D+} r(2I + d)   (DESIGN R14)
+__global__ void k_restrict(DGrid gf, DGrid gc, const double* __restrict__ rf,
+                           double* __restrict__ bc) {
+  int I, J, K;
+  if (!owned_vertex(gc, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, I, J, K)) return;
+  const int fi = 2 * I, fj = 2 * J, fk = 2 * K;
+  const int D[7][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {1, 1, 0}, {1, 0, 1}, {0, 1, 1}, {1, 1, 1}};
+  const bool dir = is_dirichlet(gc, I, J, K);
+  const int64_t oc = vidx(gc, I, J, K);
+  for (int f = 0; f < 4; ++f) {
+    if (f < 3 && dir) { bc[f * gc.fs + oc] = 0.0; continue; }
+    const double* r = rf + f * gf.fs;
+    double s = r[vidx(gf, fi, fj, fk)];
+    double e = 0.0;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      for (int sg = -1; sg <= 1; sg += 2) {
+        const int a = fi + sg * D[q][0], b = fj + sg * D[q][1], c = fk + sg * D[q][2];
+        if (a < 0 || b < 0 || c < 0 || a > gf.n || b > gf.n || c > gf.n) continue;
+        e += r[vidx(gf, a, b, c)];
+      }
+    }
+    bc[f * gc.fs + oc] = s + 0.5 * e;
+  }
+}
+
+// x_f += P x_c: fine vertex 2I + d (d in {0,1}^3) takes x_c(I) (d = 0) or the
+// mean of the coarse Kuhn edge (I, I + d)
+__global__ void k_prolong_add(DGrid gc, DGrid gf, const double* __restrict__ xc,
+                              double* __restrict__ xf) {
+  int i, j, k;
+  if (!owned_vertex(gf, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  const int64_t of = vidx(gf, i, j, k);
+  const bool dir = is_dirichlet(gf, i, j, k);
+  const int I = i >> 1, J = j >> 1, K = k >> 1;
+  const int di = i & 1, dj = j & 1, dk = k & 1;
+  const int64_t o0 = vidx(gc, I, J, K);
+  const bool mid = di | dj | dk;
+  const int64_t o1 = mid ? vidx(gc, I + di, J + dj, K + dk) : o0;
+  for (int f = 0; f < 4; ++f) {
+    if (f < 3 && dir) { xf[f * gf.fs + of] = 0.0; continue; }
+    const double v = mid ? 0.5 * (xc[f * gc.fs + o0] + xc[f * gc.fs + o1]) : xc[f * gc.fs + o0];
+    xf[f * gf.fs + of] += v;
+  }
+}
+
+// per-block partial sums for the squared norms (velocity masked) and the
+// gauge sums: out[block][0..3] = sum x_f^2, [4] = sum w p, [5] = sum w
+__global__ void k_partials(DGrid g, const double* __restrict__ x, double* __restrict__ part,
+                           int with_gauge) {
+  __shared__ double sh[6][256];
+  int i, j, k;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+       owned_vertex(g, t, i, j, k); t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = vidx(g, i, j, k);
+    const bool dir = is_dirichlet(g, i, j, k);
+    for (int f = 0; f < 4; ++f) {
+      const double v = (f < 3 && dir) ? 0.0 : x[f * g.fs + o];
+      acc[f] += v * v;
+    }
+    if (with_gauge) {
+      const double w = gauge_weight(g, i, j, k);
+      acc[4] += w * x[3 * g.fs + o];
+      acc[5] += w;
+    }
+  }
+  for (int q = 0; q < 6; ++q) sh[q][threadIdx.x] = acc[q];
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int q = 0; q < 6; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 6; ++q) part[blockIdx.x * 6 + q] = sh[q][0];
+}
+
+// fixed-order final sum of the partials (deterministic)
+__global__ void k_partials_final(const double* __restrict__ part, int nblocks,
+                                 double* __restrict__ out) {
+  __shared__ double sh[6][256];
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x)
+    for (int q = 0; q < 6; ++q) acc[q] += part[b * 6 + q];
+  for (int q = 0; q < 6; ++q) sh[q][threadIdx.x] = acc[q];
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int q = 0; q < 6; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 6; ++q) out[q] = sh[q][0];
+}
+
+// p -= (sum w p)/(sum w), sums read from device memory
+__global__ void k_gauge_apply(DGrid g, double* __restrict__ x, const double* __restrict__ sums) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  const double mean = sums[4] / sums[5];
+  x[3 * g.fs + vidx(g, i, j, k)] -= mean;
+}
+
+// nodal forcing: b_u = M f  (consistent mass, (phi_i,phi_j)_T = |T|/20 (1 + delta_ij)),
+// f in the padded level layout (fields 0..2, halo planes valid); b_p = 0; Dirichlet rows 0
+__global__ void k_load_nodal(DGrid g, const double* __restrict__ f, double* __restrict__ b) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  const double c = g.h * g.h * g.h / 6.0 / 20.0;
+  double acc[3] = {0, 0, 0};
+  auto fval = [&](int a, int ii, int jj, int kk) -> double { return f[a * g.fs + vidx(g, ii, jj, kk)]; };
+  for (int dz = -1; dz <= 0; ++dz) {
+    const int ck = k + dz;
+    if (ck < 0 || ck >= g.n) continue;
+    for (int dy = -1; dy <= 0; ++dy) {
+      const int cj = j + dy;
+      if (cj < 0 || cj >= g.n) continue;
+      for (int dx = -1; dx <= 0; ++dx) {
+        const int ci = i + dx;
+        if (ci < 0 || ci >= g.n) continue;
+        const int corner = (-dx) | ((-dy) << 1) | ((-dz) << 2);
+        for (int t = 0; t < 6; ++t) {
+          if (c_corner_m[corner][t] < 0) continue;
+          const int s1 = c_perm[t][0], s2 = c_perm[t][1];
+          int v1[3] = {ci, cj, ck}; v1[s1] += 1;
+          int v2[3] = {v1[0], v1[1], v1[2]}; v2[s2] += 1;
+          for (int a = 0; a < 3; ++a) {
+            const double sum = fval(a, ci, cj, ck) + fval(a, v1[0], v1[1], v1[2]) +
+                               fval(a, v2[0], v2[1], v2[2]) + fval(a, ci + 1, cj + 1, ck + 1);
+            acc[a] += c * (sum + fval(a, i, j, k));
+          }
+        }
+      }
+    }
+  }
+  const int64_t o = vidx(g, i, j, k);
+  const bool dir = is_dirichlet(g, i, j, k);
+  for (int a = 0; a < 3; ++a) b[a * g.fs + o] = dir ? 0.0 : acc[a];
+  b[3 * g.fs + o] = 0.0;
+}
+
+// element-constant forcing: b_{i,a} = sum_T f_{T,a} |T| / 4 ; fcls per element (same
+// layout as the viscosity classes), table [3 * nftab] in device memory
+__global__ void k_load_elem(DGrid g, const uint8_t* __restrict__ fcls,
+                            const double* __restrict__ table, double* __restrict__ b) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  const double vq = 0.25 * g.h * g.h * g.h / 6.0;
+  double acc[3] = {0, 0, 0};
+  for (int dz = -1; dz <= 0; ++dz) {
+    const int ck = k + dz;
+    if (ck < 0 || ck >= g.n) continue;
+    for (int dy = -1; dy <= 0; ++dy) {
+      const int cj = j + dy;
+      if (cj < 0 || cj >= g.n) continue;
+      for (int dx = -1; dx <= 0; ++dx) {
+        const int ci = i + dx;
+        if (ci < 0 || ci >= g.n) continue;
+        const int corner = (-dx) | ((-dy) << 1) | ((-dz) << 2);
+        for (int t = 0; t < 6; ++t) {
+          if (c_corner_m[corner][t] < 0) continue;
+          const uint8_t fc = fcls[((((int64_t)(ck - g.cz0)) * g.n + cj) * g.n + ci) * 6 + t];
+          for (int a = 0; a < 3; ++a) acc[a] += vq * table[3 * fc + a];
+        }
+      }
+    }
+  }
+  const int64_t o = vidx(g, i, j, k);
+  const bool dir = is_dirichlet(g, i, j, k);
+  for (int a = 0; a < 3; ++a) b[a * g.fs + o] = dir ? 0.0 : acc[a];
+  b[3 * g.fs + o] = 0.0;
+}
+
+// canonical (4 x (n+1)^2 x nzl, field-major) <-> padded layout
+__global__ void k_pack(DGrid g, const double* __restrict__ canon, double* __restrict__ dev,
+                       int nfields) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  const int64_t nx = g.n + 1, per = nx * nx, cs = per * g.nzl;
+  const int64_t c = (int64_t)(k - g.z0) * per + (int64_t)j * nx + i;
+  const int64_t o = vidx(g, i, j, k);
+  for (int f = 0; f < nfields; ++f) dev[f * g.fs + o] = canon[f * cs + c];
+}
+__global__ void k_unpack(DGrid g, const double* __restrict__ dev, double* __restrict__ canon) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  const int64_t nx = g.n + 1, per = nx * nx, cs = per * g.nzl;
+  const int64_t c = (int64_t)(k - g.z0) * per + (int64_t)j * nx + i;
+  const int64_t o = vidx(g, i, j, k);
+  for (int f = 0; f < 4; ++f) canon[f * cs + c] = dev[f * g.fs + o];
+}
+
+// ---- setup kernels -------------------------------------------------------
+
+// coarse element class = majority class of its 8 Bey children; ties -> larger mu,
+// then smaller class id (DESIGN R15).  gf/gc: fine/coarse grids (cube layers stored).
+__global__ void k_coarsen_classes(DGrid gf, DGrid gc, int ncz, uint8_t* __restrict__ cls_c) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int nc = gc.n;
+  const int64_t total = (int64_t)ncz * nc * nc * 6;
+  if (tid >= total) return;
+  const int T = (int)(tid % 6);
+  int64_t r = tid / 6;
+  const int CI = (int)(r % nc);
+  r /= nc;
+  const int CJ = (int)(r % nc);
+  const int CK = gc.cz0 + (int)(r / nc);
+  uint8_t cl[8];
+  int cnt[8];
+  for (int q = 0; q < 8; ++q) {
+    const int off = c_child_off[T][q];
+    cl[q] = elem_class(gf, 2 * CI + (off & 1), 2 * CJ + ((off >> 1) & 1), 2 * CK + ((off >> 2) & 1),
+                       c_child_t[T][q]);
+  }
+  for (int q = 0; q < 8; ++q) {
+    cnt[q] = 0;
+    for (int s = 0; s < 8; ++s) cnt[q] += cl[s] == cl[q];
+  }
+  int best = 0;
+  for (int q = 1; q < 8; ++q) {
+    const bool better = cnt[q] > cnt[best] ||
+                        (cnt[q] == cnt[best] && (c_mu[cl[q]] > c_mu[cl[best]] ||
+                                                 (c_mu[cl[q]] == c_mu[cl[best]] && cl[q] < cl[best])));
+    if (better) best = q;
+  }
+  cls_c[tid] = cl[best];
+}
+
+// per-vertex code: regular class k (interior vertex whose 24 incident tets share
+// mu_k) or CODE_IRREGULAR (interface Gamma_12, boundary / Gamma_F rows);
+// counts irregular vertices into *nirr
+__global__ void k_classify(DGrid g, uint8_t* __restrict__ code, unsigned long long* nirr) {
+  int i, j, k;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (!owned_vertex(g, tid, i, j, k)) return;
+  uint8_t c = CODE_IRREGULAR;
+  if (i > 0 && j > 0 && k > 0 && i < g.n && j < g.n && k < g.n) {
+    bool same = true;
+    int first = -1;
+    for (int dz = -1; dz <= 0; ++dz)
+      for (int dy = -1; dy <= 0; ++dy)
+        for (int dx = -1; dx <= 0; ++dx) {
+          const int corner = (-dx) | ((-dy) << 1) | ((-dz) << 2);
+          for (int t = 0; t < 6; ++t) {
+            if (c_corner_m[corner][t] < 0) continue;
+            const int cl = elem_class(g, i + dx, j + dy, k + dz, t);
+            if (first < 0) first = cl;
+            else if (cl != first && c_mu[cl] != c_mu[first]) same = false;
+          }
+        }
+    if (same) c = (uint8_t)first;
+  }
+  code[vidx(g, i, j, k)] = c;
+  if (c == CODE_IRREGULAR) atomicAdd(nirr, 1ull);
+}
+
+// ---- coarsest level: dense assembly, Gauss-Jordan inverse, apply -----------
+
+struct FetchUnit {
+  int ui, uj, uk, uf;
+  __device__ __forceinline__ double operator()(const DGrid& g, int i, int j, int k, int f) const {
+    return (i == ui && j == uj && k == uk && f == uf) ? 1.0 : 0.0;
+  }
+};
+
+// K[r][c] = row r of K applied to the unit vector of free DoF c; N1 = leading dim.
+// dofs[q] = (f << 28) | (k << 18) | (j << 9) | i  (global coordinates)
+template <int FORM>
+__global__ void k_coarse_assemble(DGrid g, const int32_t* __restrict__ dofs, int N, int N1,
+                                  double* __restrict__ K, int gauge) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid >= (int64_t)N1 * N1) return;
+  const int r = (int)(tid / N1), c = (int)(tid % N1);
+  double v = 0.0;
+  auto unpack = [](int32_t d, int& f, int& i, int& j, int& k) {
+    f = (d >> 28) & 0xF; k = (d >> 18) & 0x3FF; j = (d >> 9) & 0x1FF; i = d & 0x1FF;
+  };
+  if (r < N && c < N) {
+    int fr, ir, jr, kr, fc, ic, jc, kc;
+    unpack(dofs[r], fr, ir, jr, kr);
+    unpack(dofs[c], fc, ic, jc, kc);
+    if (abs(ir - ic) <= 1 && abs(jr - jc) <= 1 && abs(kr - kc) <= 1) {
+      FetchUnit fx{ic, jc, kc, fc};
+      double y[4], dA[3], dC;
+      row_generic<FORM>(g, ir, jr, kr, fx, BLK_ALL, y, dA, dC);
+      v = y[fr];
+    }
+  } else if (gauge && (r < N || c < N) && !(r == N && c == N)) {
+    const int q = r < N ? r : c;
+    int f, i, j, k;
+    unpack(dofs[q], f, i, j, k);
+    v = f == 3 ? gauge_weight(g, i, j, k) : 0.0;
+  }
+  K[(int64_t)r * N1 + c] = v;
+}
+
+// In-place Gauss-Jordan inverse with partial pivoting of an N x N matrix (one block).
+__global__ void k_gauss_jordan(double* __restrict__ A, double* __restrict__ Inv, int N,
+                               int* __restrict__ status) {
+  __shared__ int piv;
+  __shared__ double redv[1024];
+  __shared__ int redi[1024];
+  for (int64_t e = threadIdx.x; e < (int64_t)N * N; e += blockDim.x)
+    Inv[e] = (e / N == e % N) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int c = 0; c < N; ++c) {
+    double best = -1.0;
+    int bi = c;
+    for (int r = c + threadIdx.x; r < N; r += blockDim.x) {
+      const double v = fabs(A[(int64_t)r * N + c]);
+      if (v > best) { best = v; bi = r; }
+    }
+    redv[threadIdx.x] = best;
+    redi[threadIdx.x] = bi;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if (threadIdx.x < s && (redv[threadIdx.x + s] > redv[threadIdx.x] ||
+                              (redv[threadIdx.x + s] == redv[threadIdx.x] &&
+                               redi[threadIdx.x + s] < redi[threadIdx.x]))) {
+        redv[threadIdx.x] = redv[threadIdx.x + s];
+        redi[threadIdx.x] = redi[threadIdx.x + s];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      piv = redi[0];
+      if (!(redv[0] > 0.0)) *status = 1;
+    }
+    __syncthreads();
+    const int p = piv;
+    if (p != c) {
+      for (int q = threadIdx.x; q < N; q += blockDim.x) {
+        double t = A[(int64_t)c * N + q]; A[(int64_t)c * N + q] = A[(int64_t)p * N + q]; A[(int64_t)p * N + q] = t;
+        t = Inv[(int64_t)c * N + q]; Inv[(int64_t)c * N + q] = Inv[(int64_t)p * N + q]; Inv[(int64_t)p * N + q] = t;
+      }
+    }
+    __syncthreads();
+    const double d = A[(int64_t)c * N + c];
+    __syncthreads();
+    for (int q = threadIdx.x; q < N; q += blockDim.x) {
+      A[(int64_t)c * N + q] /= d;
+      Inv[(int64_t)c * N + q] /= d;
+    }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < (int64_t)N * N; e += blockDim.x) {
+      const int r = (int)(e / N), q = (int)(e % N);
+      if (r == c || q == c) continue;
+      const double fct = A[(int64_t)r * N + c];
+      A[e] -= fct * A[(int64_t)c * N + q];
+      Inv[e] -= fct * Inv[(int64_t)c * N + q];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < N; r += blockDim.x) {
+      if (r == c) continue;
+      const double fct = A[(int64_t)r * N + c];
+      Inv[(int64_t)r * N + c] -= fct * Inv[(int64_t)c * N + c];
+      A[(int64_t)r * N + c] = 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+// x_F = G b_F on the coarsest level (G: N x N with leading dimension ld); other entries 0
+__global__ void k_coarse_apply(DGrid g, const int32_t* __restrict__ dofs, int N, int ld,
+                               const double* __restrict__ G, const double* __restrict__ b,
+                               double* __restrict__ x) {
+  extern __shared__ double bs[];
+  for (int q = threadIdx.x; q < N; q += blockDim.x) {
+    const int32_t d = dofs[q];
+    const int f = (d >> 28) & 0xF, k = (d >> 18) & 0x3FF, j = (d >> 9) & 0x1FF, i = d & 0x1FF;
+    bs[q] = b[f * g.fs + vidx(g, i, j, k)];
+  }
+  __syncthreads();
+  // zero everything first (Dirichlet entries), then write free entries
+  const int64_t nx = g.n + 1;
+  for (int64_t e = threadIdx.x; e < nx * nx * g.nzl; e += blockDim.x) {
+    const int i = (int)(e % nx), j = (int)((e / nx) % nx), k = g.z0 + (int)(e / (nx * nx));
+    for (int f = 0; f < 4; ++f) x[f * g.fs + vidx(g, i, j, k)] = 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < N; r += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < N; ++c) s += G[(int64_t)r * ld + c] * bs[c];
+    const int32_t d = dofs[r];
+    const int f = (d >> 28) & 0xF, k = (d >> 18) & 0x3FF, j = (d >> 9) & 0x1FF, i = d & 0x1FF;
+    x[f * g.fs + vidx(g, i, j, k)] = s;
+  }
+}
+
+}  // namespace stk

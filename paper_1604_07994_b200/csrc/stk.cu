@@ -1,0 +1,781 @@
+// stk.cu — C ABI (include/stk.h) of the B200 Stokes operator / Uzawa multigrid.
+//
+// One translation unit: the device headers define __constant__ tables that all
+// kernels share.  Host code here is setup + launch orchestration only; every
+// step of the solver path runs in the kernels of kernels_*.cuh.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/stk.h"
+#include "comm.cuh"
+#include "kernels_generic.cuh"
+#include "kernels_tiled.cuh"
+
+using namespace stk;
+
+namespace {
+
+struct Level {
+  int n = 0;
+  double h = 0;
+  int z0 = 0, nzl = 0;   // owned vertex planes
+  int cz0 = 0, cz1 = 0;  // stored cube layers
+  int64_t px = 0, py = 0, fs = 0, vlen = 0;
+  uint8_t* cls = nullptr;
+  uint8_t* code = nullptr;
+  double* x = nullptr;    // MG iterate (levels >= 1)
+  double* b = nullptr;    // MG rhs (levels >= 1)
+  double* r = nullptr;    // scratch: residual / smoother temporaries
+  int64_t nirr = 0;
+  bool replicated = false;  // whole level held by every rank (coarse agglomeration)
+};
+
+}  // namespace
+
+struct stk_ctx {
+  stk_config cfg{};
+  cudaStream_t stream = nullptr;
+  int nlev = 0;
+  std::vector<Level> lev;
+  int state = 0;  // 0 created, 1 viscosity set, 2 assembled
+  std::vector<double> class_mu;
+  std::string err;
+  int kernel_mode = 1;
+  int64_t launches = 0;
+  // coarsest level
+  int32_t* cdofs = nullptr;
+  int cN = 0, cN1 = 0;
+  double* cK = nullptr;
+  double* cG = nullptr;
+  int* cstatus = nullptr;
+  // reductions
+  double* part = nullptr;
+  double* sums = nullptr;
+  double* hsums = nullptr;  // pinned
+  int nparts = 0;
+  Comm comm;
+};
+
+namespace {
+
+constexpr int kThreads = 256;
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);               \
+      return STK_ECUDA;                                                            \
+    }                                                                              \
+  } while (0)
+
+#define ST(call)                      \
+  do {                                \
+    stk_status s_ = (call);           \
+    if (s_ != STK_OK) return s_;      \
+  } while (0)
+
+stk_status launched(stk_ctx* ctx) {
+  ctx->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    ctx->err = std::string("kernel launch: ") + cudaGetErrorString(e);
+    return STK_ECUDA;
+  }
+  return STK_OK;
+}
+
+unsigned dirmask_of(const stk_config& c) {
+  unsigned m = 0;
+  for (int f = 0; f < 6; ++f)
+    if (c.face[f] == STK_FACE_DIRICHLET0) m |= 1u << f;
+  return m;
+}
+
+DGrid dgrid(const stk_ctx* ctx, const Level& L) {
+  DGrid g;
+  g.n = L.n;
+  g.z0 = L.z0;
+  g.nzl = L.nzl;
+  g.cz0 = L.cz0;
+  g.px = L.px;
+  g.py = L.py;
+  g.fs = L.fs;
+  g.h = L.h;
+  g.delta = ctx->cfg.delta;
+  g.dirmask = dirmask_of(ctx->cfg);
+  g.cls = L.cls;
+  g.code = L.code;
+  return g;
+}
+
+int64_t owned_vertices(const Level& L) { return (int64_t)(L.n + 1) * (L.n + 1) * L.nzl; }
+unsigned nblocks(int64_t work) { return (unsigned)((work + kThreads - 1) / kThreads); }
+
+bool has_traction(const stk_config& c) {
+  for (int f = 0; f < 6; ++f)
+    if (c.face[f] == STK_FACE_TRACTION) return true;
+  return false;
+}
+
+void host_tables(int8_t perm[6][3], int8_t corner[8][6], int8_t choff[6][8], int8_t cht[6][8]) {
+  const int P[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  for (int t = 0; t < 6; ++t) {
+    for (int d = 0; d < 3; ++d) perm[t][d] = (int8_t)P[t][d];
+    // vertex offsets a0..a3 as corner bits
+    int a[4];
+    a[0] = 0;
+    a[1] = 1 << P[t][0];
+    a[2] = a[1] | (1 << P[t][1]);
+    a[3] = 7;
+    for (int c = 0; c < 8; ++c) {
+      corner[c][t] = -1;
+      for (int m = 0; m < 4; ++m)
+        if (a[m] == c) corner[c][t] = (int8_t)m;
+    }
+  }
+  // Bey children: fine tet (cube offset o, type t) lies in coarse tet T iff its
+  // centroid q (coarse-cube units) satisfies q[sT1] > q[sT2] > q[sT3].
+  for (int T = 0; T < 6; ++T) {
+    int cnt = 0;
+    for (int o = 0; o < 8; ++o)
+      for (int t = 0; t < 6; ++t) {
+        double q[3];
+        for (int d = 0; d < 3; ++d) q[d] = (o >> d) & 1;
+        q[P[t][0]] += 0.75;
+        q[P[t][1]] += 0.5;
+        q[P[t][2]] += 0.25;
+        for (int d = 0; d < 3; ++d) q[d] *= 0.5;
+        if (q[P[T][0]] > q[P[T][1]] && q[P[T][1]] > q[P[T][2]]) {
+          choff[T][cnt] = (int8_t)o;
+          cht[T][cnt] = (int8_t)t;
+          ++cnt;
+        }
+      }
+    if (cnt != 8) fprintf(stderr, "stk: Bey child table broken (%d)\n", cnt);
+  }
+}
+
+template <class K1, class K2, class K3>
+void pick_form(int form, K1 k_mod, K2 k_sym, K3 k_grad);
+
+// ---- level operations ------------------------------------------------------
+
+bool use_tiled(const stk_ctx* ctx, const Level& L) {
+  return ctx->kernel_mode == 1 && L.n >= 64 && !L.replicated && tiled_supported(L.n);
+}
+
+stk_status op_apply(stk_ctx* ctx, int l, unsigned blocks, const double* x, double* y) {
+  Level& L = ctx->lev[l];
+  ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, const_cast<double*>(x), 0, 4, L.replicated));
+  DGrid g = dgrid(ctx, L);
+  if (use_tiled(ctx, L)) {
+    ST(launch_apply_tiled(ctx->cfg.form, g, x, y, blocks, ctx->stream) ? STK_OK : STK_EUNSUP);
+    return launched(ctx);
+  }
+  const unsigned nb = nblocks(owned_vertices(L));
+  switch (ctx->cfg.form) {
+    case FORM_MOD: k_apply_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, x, y, blocks); break;
+    case FORM_SYM: k_apply_generic<FORM_SYM><<<nb, kThreads, 0, ctx->stream>>>(g, x, y, blocks); break;
+    default: k_apply_generic<FORM_GRAD><<<nb, kThreads, 0, ctx->stream>>>(g, x, y, blocks); break;
+  }
+  return launched(ctx);
+}
+
+stk_status op_residual(stk_ctx* ctx, int l, const double* x, const double* b, double* r) {
+  Level& L = ctx->lev[l];
+  ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, const_cast<double*>(x), 0, 4, L.replicated));
+  DGrid g = dgrid(ctx, L);
+  if (use_tiled(ctx, L)) {
+    ST(launch_residual_tiled(ctx->cfg.form, g, x, b, r, ctx->stream) ? STK_OK : STK_EUNSUP);
+    return launched(ctx);
+  }
+  const unsigned nb = nblocks(owned_vertices(L));
+  switch (ctx->cfg.form) {
+    case FORM_MOD: k_residual_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, x, b, r); break;
+    case FORM_SYM: k_residual_generic<FORM_SYM><<<nb, kThreads, 0, ctx->stream>>>(g, x, b, r); break;
+    default: k_residual_generic<FORM_GRAD><<<nb, kThreads, 0, ctx->stream>>>(g, x, b, r); break;
+  }
+  return launched(ctx);
+}
+
+// one Uzawa step in place on x (4 fields), rhs b; scratch L.r
+stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
+  Level& L = ctx->lev[l];
+  DGrid g = dgrid(ctx, L);
+  const int nc = ctx->cfg.ncolors_u;
+  const unsigned nb = nblocks(owned_vertices(L));
+  double* tmp = L.r;  // fields 0..2: velocity ping-pong, field 3: pressure temp T
+  double* p = x + 3 * L.fs;
+  const bool tiled = use_tiled(ctx, L);
+  // pressure halo is fixed during the velocity sweep
+  ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, x, 3, 1, L.replicated));
+  int pass = 0;
+  for (int s = 0; s < 2 * nc; ++s, ++pass) {
+    const int color = s < nc ? s : 2 * nc - 1 - s;
+    const double* uin = (pass & 1) ? tmp : x;
+    double* uout = (pass & 1) ? x : tmp;
+    ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, const_cast<double*>(uin), 0, 3, L.replicated));
+    if (tiled) {
+      ST(launch_vel_pass_tiled(ctx->cfg.form, g, uin, p, b, uout, color, nc, ctx->stream) ? STK_OK
+                                                                                           : STK_EUNSUP);
+    } else {
+      switch (ctx->cfg.form) {
+        case FORM_MOD: k_vel_pass_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, uin, p, b, uout, color, nc); break;
+        case FORM_SYM: k_vel_pass_generic<FORM_SYM><<<nb, kThreads, 0, ctx->stream>>>(g, uin, p, b, uout, color, nc); break;
+        default: k_vel_pass_generic<FORM_GRAD><<<nb, kThreads, 0, ctx->stream>>>(g, uin, p, b, uout, color, nc); break;
+      }
+    }
+    ST(launched(ctx));
+  }
+  // 2*nc passes: result is back in x
+  ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, x, 0, 3, L.replicated));
+  double* T = tmp + 3 * L.fs;
+  const double* gp = b + 3 * L.fs;
+  if (tiled) {
+    ST(launch_p_pass1_tiled(ctx->cfg.form, g, x, gp, T, ctx->stream) ? STK_OK : STK_EUNSUP);
+  } else {
+    switch (ctx->cfg.form) {
+      case FORM_MOD: k_p_pass1_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, x, gp, T); break;
+      case FORM_SYM: k_p_pass1_generic<FORM_SYM><<<nb, kThreads, 0, ctx->stream>>>(g, x, gp, T); break;
+      default: k_p_pass1_generic<FORM_GRAD><<<nb, kThreads, 0, ctx->stream>>>(g, x, gp, T); break;
+    }
+  }
+  ST(launched(ctx));
+  ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, tmp, 3, 1, L.replicated));
+  if (tiled) {
+    ST(launch_p_pass2_tiled(g, T, p, ctx->cfg.omega, ctx->stream) ? STK_OK : STK_EUNSUP);
+  } else {
+    k_p_pass2_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, T, p, ctx->cfg.omega);
+  }
+  return launched(ctx);
+}
+
+stk_status op_restrict(stk_ctx* ctx, int lf, const double* rf, double* bc) {
+  Level& F = ctx->lev[lf];
+  Level& C = ctx->lev[lf + 1];
+  ST(ctx->comm.halo(ctx, F.n, F.z0, F.nzl, F.py, F.fs, const_cast<double*>(rf), 0, 4, F.replicated));
+  if (C.replicated && !F.replicated) {
+    // distributed fine level -> replicated coarse level: restrict locally into the
+    // owned coarse planes, then gather the coarse planes of all ranks
+    ST(ctx->comm.restrict_to_replicated(ctx, dgrid(ctx, F), dgrid(ctx, C), rf, bc));
+    return STK_OK;
+  }
+  k_restrict<<<nblocks(owned_vertices(C)), kThreads, 0, ctx->stream>>>(dgrid(ctx, F), dgrid(ctx, C), rf, bc);
+  return launched(ctx);
+}
+
+stk_status op_prolong_add(stk_ctx* ctx, int lc, const double* xc, double* xf) {
+  Level& C = ctx->lev[lc];
+  Level& F = ctx->lev[lc - 1];
+  ST(ctx->comm.halo(ctx, C.n, C.z0, C.nzl, C.py, C.fs, const_cast<double*>(xc), 0, 4, C.replicated));
+  DGrid gc = dgrid(ctx, C);
+  if (C.replicated && !F.replicated) gc = ctx->comm.replicated_view(gc);
+  k_prolong_add<<<nblocks(owned_vertices(F)), kThreads, 0, ctx->stream>>>(gc, dgrid(ctx, F), xc, xf);
+  return launched(ctx);
+}
+
+stk_status op_coarse(stk_ctx* ctx, const double* b, double* x) {
+  Level& L = ctx->lev[ctx->nlev - 1];
+  const size_t sh = sizeof(double) * ctx->cN;
+  k_coarse_apply<<<1, 1024, sh, ctx->stream>>>(dgrid(ctx, L), ctx->cdofs, ctx->cN, ctx->cN1, ctx->cG, b, x);
+  return launched(ctx);
+}
+
+// squared norms (+ gauge sums) of a level vector, summed over ranks, into ctx->sums (device)
+stk_status op_partials(stk_ctx* ctx, int l, const double* x, int with_gauge) {
+  Level& L = ctx->lev[l];
+  DGrid g = dgrid(ctx, L);
+  k_partials<<<ctx->nparts, 256, 0, ctx->stream>>>(g, x, ctx->part, with_gauge);
+  ST(launched(ctx));
+  k_partials_final<<<1, 256, 0, ctx->stream>>>(ctx->part, ctx->nparts, ctx->sums);
+  ST(launched(ctx));
+  if (!L.replicated) ST(ctx->comm.allreduce_sum(ctx, ctx->sums, 6));
+  return STK_OK;
+}
+
+stk_status op_gauge(stk_ctx* ctx, int l, double* x) {
+  if (has_traction(ctx->cfg)) return STK_OK;
+  Level& L = ctx->lev[l];
+  ST(op_partials(ctx, l, x, 1));
+  k_gauge_apply<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), x, ctx->sums);
+  return launched(ctx);
+}
+
+stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x) {
+  if (l == ctx->nlev - 1) return op_coarse(ctx, b, x);
+  Level& L = ctx->lev[l];
+  Level& C = ctx->lev[l + 1];
+  const int nu_pre = ctx->cfg.nu_pre + ctx->cfg.nu_inc * l;
+  const int nu_post = ctx->cfg.nu_post + ctx->cfg.nu_inc * l;
+  for (int s = 0; s < nu_pre; ++s) ST(op_uzawa(ctx, l, x, b));
+  ST(op_residual(ctx, l, x, b, L.r));
+  ST(op_restrict(ctx, l, L.r, C.b));
+  CK(cudaMemsetAsync(C.x, 0, sizeof(double) * C.vlen, ctx->stream));
+  ST(op_vcycle(ctx, l + 1, C.b, C.x));
+  ST(op_prolong_add(ctx, l + 1, C.x, x));
+  for (int s = 0; s < nu_post; ++s) ST(op_uzawa(ctx, l, x, b));
+  return STK_OK;
+}
+
+stk_status check(const stk_ctx* ctx, int need_state) {
+  if (!ctx) return STK_EINVAL;
+  if (ctx->state < need_state) {
+    const_cast<stk_ctx*>(ctx)->err = "call order violated (create -> set_viscosity -> assemble)";
+    return STK_ESTATE;
+  }
+  return STK_OK;
+}
+
+stk_status check_level(stk_ctx* ctx, int l) {
+  if (l < 0 || l >= ctx->nlev) {
+    ctx->err = "level out of range";
+    return STK_EINVAL;
+  }
+  return STK_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+extern "C" {
+
+stk_status stk_nccl_unique_id(uint8_t id[128]) { return comm_unique_id(id); }
+
+stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
+  if (!cfg || !out) return STK_EINVAL;
+  *out = nullptr;
+  const int n = cfg->n;
+  if (n < 4 || (n & (n - 1)) != 0) return STK_EINVAL;
+  if (cfg->form < 0 || cfg->form > 2) return STK_EINVAL;
+  if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return STK_EINVAL;
+  if (cfg->ncolors_u != 2 && cfg->ncolors_u != 4) return STK_EINVAL;
+  const int nc = cfg->n_coarse > 0 ? cfg->n_coarse : 4;
+  if (nc > n || (nc & (nc - 1)) != 0 || nc > 16) return STK_EINVAL;
+  bool any_dir = false;
+  for (int f = 0; f < 6; ++f) {
+    if (cfg->face[f] != STK_FACE_DIRICHLET0 && cfg->face[f] != STK_FACE_TRACTION) return STK_EINVAL;
+    any_dir |= cfg->face[f] == STK_FACE_DIRICHLET0;
+  }
+  if (!any_dir) return STK_EINVAL;  // Korn: |Gamma_D| > 0
+  stk_ctx* ctx = new stk_ctx();
+  ctx->cfg = *cfg;
+  ctx->cfg.n_coarse = nc;
+  if (ctx->cfg.delta <= 0) ctx->cfg.delta = 1.0 / 12.0;
+  ctx->stream = (cudaStream_t)cfg->stream;
+  // constant tables
+  int8_t perm[6][3], corner[8][6], choff[6][8], cht[6][8];
+  host_tables(perm, corner, choff, cht);
+  auto fail = [&](stk_status s) { *out = ctx; return s; };
+  if (cudaMemcpyToSymbol(c_perm, perm, sizeof(perm)) != cudaSuccess ||
+      cudaMemcpyToSymbol(c_corner_m, corner, sizeof(corner)) != cudaSuccess ||
+      cudaMemcpyToSymbol(c_child_off, choff, sizeof(choff)) != cudaSuccess ||
+      cudaMemcpyToSymbol(c_child_t, cht, sizeof(cht)) != cudaSuccess) {
+    ctx->err = "cudaMemcpyToSymbol failed (no CUDA device?)";
+    return fail(STK_ECUDA);
+  }
+  // communicator
+  stk_status s = ctx->comm.init(ctx, cfg->rank, cfg->nranks, id);
+  if (s != STK_OK) return fail(s);
+  // levels
+  for (int m = n; m >= nc; m /= 2) {
+    Level L;
+    L.n = m;
+    L.h = 1.0 / m;
+    ctx->lev.push_back(L);
+  }
+  ctx->nlev = (int)ctx->lev.size();
+  for (int l = 0; l < ctx->nlev; ++l) {
+    Level& L = ctx->lev[l];
+    const int P = cfg->nranks;
+    L.replicated = !(P == 1 || (L.n % P == 0 && L.n / P >= 2 && l < ctx->nlev - 1));
+    if (l > 0 && ctx->lev[l - 1].replicated) L.replicated = true;
+    if (!L.replicated && P > 1) {
+      // distributed levels need their coarse partner planes on the same rank
+      if ((L.n / P) % 2 != 0 && l + 1 < ctx->nlev) {
+        // next level becomes replicated (handled by its own flag)
+      }
+    }
+    const int r = L.replicated ? 0 : cfg->rank;
+    const int Pn = L.replicated ? 1 : P;
+    const int per = L.n / Pn;
+    L.z0 = r * per;
+    L.nzl = per + (r == Pn - 1 ? 1 : 0);
+    L.cz0 = std::max(0, L.z0 - 1);
+    L.cz1 = std::min(L.n, L.z0 + L.nzl);
+    L.px = ((L.n + 1 + 15) / 16) * 16;
+    L.py = L.px * (L.n + 1);
+    L.fs = (((int64_t)(L.nzl + 2) * L.py + 31) / 32) * 32;
+    L.vlen = 4 * L.fs;
+    const size_t ncls = (size_t)(L.cz1 - L.cz0) * L.n * L.n * 6;
+    if (cudaMalloc(&L.cls, ncls) != cudaSuccess ||
+        cudaMalloc(&L.code, sizeof(uint8_t) * L.fs) != cudaSuccess ||
+        cudaMalloc(&L.r, sizeof(double) * L.vlen) != cudaSuccess) {
+      ctx->err = "out of device memory (level arrays)";
+      return fail(STK_ENOMEM);
+    }
+    cudaMemset(L.r, 0, sizeof(double) * L.vlen);
+    cudaMemset(L.code, CODE_IRREGULAR, L.fs);
+    if (l > 0) {
+      if (cudaMalloc(&L.x, sizeof(double) * L.vlen) != cudaSuccess ||
+          cudaMalloc(&L.b, sizeof(double) * L.vlen) != cudaSuccess) {
+        ctx->err = "out of device memory (MG vectors)";
+        return fail(STK_ENOMEM);
+      }
+      cudaMemset(L.x, 0, sizeof(double) * L.vlen);
+      cudaMemset(L.b, 0, sizeof(double) * L.vlen);
+    }
+  }
+  ctx->nparts = 296;
+  if (cudaMalloc(&ctx->part, sizeof(double) * 6 * ctx->nparts) != cudaSuccess ||
+      cudaMalloc(&ctx->sums, sizeof(double) * 8) != cudaSuccess ||
+      cudaMallocHost(&ctx->hsums, sizeof(double) * 8) != cudaSuccess ||
+      cudaMalloc(&ctx->cstatus, sizeof(int)) != cudaSuccess) {
+    ctx->err = "allocation failed";
+    return fail(STK_ENOMEM);
+  }
+  *out = ctx;
+  return STK_OK;
+}
+
+stk_status stk_cube_range(const stk_ctx* ctx, int32_t* z0, int32_t* z1) {
+  if (!ctx || !z0 || !z1) return STK_EINVAL;
+  *z0 = ctx->lev[0].cz0;
+  *z1 = ctx->lev[0].cz1;
+  return STK_OK;
+}
+
+stk_status stk_set_viscosity(stk_ctx* ctx, const uint8_t* elem_class, const double* class_mu,
+                             int32_t nclass) {
+  ST(check(ctx, 0));
+  if (!elem_class || !class_mu || nclass < 1 || nclass > 255) return STK_EINVAL;
+  double mu[256], imu[256];
+  for (int q = 0; q < 256; ++q) mu[q] = imu[q] = 1.0;
+  for (int q = 0; q < nclass; ++q) {
+    if (!(class_mu[q] > 0.0)) {
+      ctx->err = "viscosities must be positive";
+      return STK_EINVAL;
+    }
+    mu[q] = class_mu[q];
+    imu[q] = 1.0 / class_mu[q];
+  }
+  ctx->class_mu.assign(class_mu, class_mu + nclass);
+  CK(cudaMemcpyToSymbolAsync(c_mu, mu, sizeof(mu), 0, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyToSymbolAsync(c_inv_mu, imu, sizeof(imu), 0, cudaMemcpyHostToDevice, ctx->stream));
+  Level& L = ctx->lev[0];
+  const size_t ncls = (size_t)(L.cz1 - L.cz0) * L.n * L.n * 6;
+  CK(cudaMemcpyAsync(L.cls, elem_class, ncls, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->state = std::max(ctx->state, 1);
+  if (ctx->state > 1) ctx->state = 1;  // re-assemble required
+  return STK_OK;
+}
+
+stk_status stk_assemble(stk_ctx* ctx) {
+  ST(check(ctx, 1));
+  // coarse classes
+  for (int l = 1; l < ctx->nlev; ++l) {
+    Level& F = ctx->lev[l - 1];
+    Level& C = ctx->lev[l];
+    if (C.replicated && !F.replicated) {
+      ST(ctx->comm.gather_classes(ctx, dgrid(ctx, F), dgrid(ctx, C), C.cls));
+    } else {
+      const int ncz = C.cz1 - C.cz0;
+      const int64_t tot = (int64_t)ncz * C.n * C.n * 6;
+      k_coarsen_classes<<<nblocks(tot), kThreads, 0, ctx->stream>>>(dgrid(ctx, F), dgrid(ctx, C), ncz, C.cls);
+      ST(launched(ctx));
+    }
+  }
+  // classification
+  unsigned long long* dcnt;
+  CK(cudaMalloc(&dcnt, sizeof(unsigned long long) * ctx->nlev));
+  CK(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * ctx->nlev, ctx->stream));
+  for (int l = 0; l < ctx->nlev; ++l) {
+    Level& L = ctx->lev[l];
+    k_classify<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), L.code, dcnt + l);
+    ST(launched(ctx));
+  }
+  std::vector<unsigned long long> cnt(ctx->nlev);
+  CK(cudaMemcpyAsync(cnt.data(), dcnt, sizeof(unsigned long long) * ctx->nlev, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(dcnt);
+  for (int l = 0; l < ctx->nlev; ++l) ctx->lev[l].nirr = (int64_t)cnt[l];
+  // constant subdomain stencils for the tiled kernels
+  for (int l = 0; l < ctx->nlev; ++l) {
+    Level& L = ctx->lev[l];
+    if (L.n >= 64) ST(assemble_stencils(ctx->cfg.form, L.h, ctx->cfg.delta, l, ctx->stream) ? STK_OK : STK_ECUDA);
+  }
+  // coarsest level: dense K (+ gauge row), Gauss-Jordan inverse
+  Level& L = ctx->lev[ctx->nlev - 1];
+  std::vector<int32_t> dofs;
+  const unsigned dm = dirmask_of(ctx->cfg);
+  for (int k = L.z0; k < L.z0 + L.nzl; ++k)
+    for (int j = 0; j <= L.n; ++j)
+      for (int i = 0; i <= L.n; ++i) {
+        const bool dir = ((dm & 1) && i == 0) || ((dm & 2) && i == L.n) || ((dm & 4) && j == 0) ||
+                         ((dm & 8) && j == L.n) || ((dm & 16) && k == 0) || ((dm & 32) && k == L.n);
+        for (int f = 0; f < 4; ++f)
+          if (f == 3 || !dir) dofs.push_back((f << 28) | (k << 18) | (j << 9) | i);
+      }
+  std::sort(dofs.begin(), dofs.end(), [](int32_t a, int32_t b) {
+    const int fa = (a >> 28) & 0xF, fb = (b >> 28) & 0xF;
+    if (fa != fb) return fa < fb;
+    return (a & 0x0FFFFFFF) < (b & 0x0FFFFFFF);
+  });
+  const bool gauge = !has_traction(ctx->cfg);
+  ctx->cN = (int)dofs.size();
+  ctx->cN1 = ctx->cN + (gauge ? 1 : 0);
+  const int N1 = ctx->cN1;
+  cudaFree(ctx->cdofs);
+  cudaFree(ctx->cK);
+  cudaFree(ctx->cG);
+  CK(cudaMalloc(&ctx->cdofs, sizeof(int32_t) * ctx->cN));
+  CK(cudaMalloc(&ctx->cK, sizeof(double) * N1 * N1));
+  CK(cudaMalloc(&ctx->cG, sizeof(double) * N1 * N1));
+  CK(cudaMemcpyAsync(ctx->cdofs, dofs.data(), sizeof(int32_t) * ctx->cN, cudaMemcpyHostToDevice, ctx->stream));
+  DGrid g = dgrid(ctx, L);
+  const unsigned nb = nblocks((int64_t)N1 * N1);
+  switch (ctx->cfg.form) {
+    case FORM_MOD: k_coarse_assemble<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, ctx->cdofs, ctx->cN, N1, ctx->cK, gauge); break;
+    case FORM_SYM: k_coarse_assemble<FORM_SYM><<<nb, kThreads, 0, ctx->stream>>>(g, ctx->cdofs, ctx->cN, N1, ctx->cK, gauge); break;
+    default: k_coarse_assemble<FORM_GRAD><<<nb, kThreads, 0, ctx->stream>>>(g, ctx->cdofs, ctx->cN, N1, ctx->cK, gauge); break;
+  }
+  ST(launched(ctx));
+  CK(cudaMemsetAsync(ctx->cstatus, 0, sizeof(int), ctx->stream));
+  k_gauss_jordan<<<1, 1024, 0, ctx->stream>>>(ctx->cK, ctx->cG, N1, ctx->cstatus);
+  ST(launched(ctx));
+  int hs = 0;
+  CK(cudaMemcpyAsync(&hs, ctx->cstatus, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hs) {
+    ctx->err = "coarse-level matrix is singular";
+    return STK_ECUDA;
+  }
+  ctx->state = 2;
+  return STK_OK;
+}
+
+stk_status stk_layout(const stk_ctx* ctx, int32_t level, stk_layout_t* out) {
+  if (!ctx || !out || level < 0 || level >= ctx->nlev) return STK_EINVAL;
+  const Level& L = ctx->lev[level];
+  out->n = L.n;
+  out->nx = out->ny = L.n + 1;
+  out->nz_local = L.nzl;
+  out->z0 = L.z0;
+  out->pitch_x = L.px;
+  out->pitch_y = L.py;
+  out->field_stride = L.fs;
+  out->vec_len = L.vlen;
+  out->n_irregular = L.nirr;
+  out->n_vertices = owned_vertices(L);
+  return STK_OK;
+}
+
+stk_status stk_import(stk_ctx* ctx, int32_t level, const double* canon, int32_t where, double* dev) {
+  ST(check(ctx, 0));
+  ST(check_level(ctx, level));
+  Level& L = ctx->lev[level];
+  const size_t bytes = sizeof(double) * 4 * owned_vertices(L);
+  const double* src = canon;
+  double* staging = nullptr;
+  if (where == STK_HOST) {
+    CK(cudaMallocAsync(&staging, bytes, ctx->stream));
+    CK(cudaMemcpyAsync(staging, canon, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    src = staging;
+  }
+  k_pack<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), src, dev, 4);
+  stk_status s = launched(ctx);
+  if (staging) CK(cudaFreeAsync(staging, ctx->stream));
+  if (where == STK_HOST) CK(cudaStreamSynchronize(ctx->stream));
+  return s;
+}
+
+stk_status stk_export(stk_ctx* ctx, int32_t level, const double* dev, double* canon, int32_t where) {
+  ST(check(ctx, 0));
+  ST(check_level(ctx, level));
+  Level& L = ctx->lev[level];
+  const size_t bytes = sizeof(double) * 4 * owned_vertices(L);
+  double* dst = canon;
+  double* staging = nullptr;
+  if (where == STK_HOST) {
+    CK(cudaMallocAsync(&staging, bytes, ctx->stream));
+    dst = staging;
+  }
+  k_unpack<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), dev, dst);
+  ST(launched(ctx));
+  if (where == STK_HOST) {
+    CK(cudaMemcpyAsync(canon, staging, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaFreeAsync(staging, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return STK_OK;
+}
+
+stk_status stk_load_vector(stk_ctx* ctx, int32_t kind, const void* f_dev, const double* table,
+                           int32_t nftab, double* b_dev) {
+  ST(check(ctx, 1));
+  Level& L = ctx->lev[0];
+  DGrid g = dgrid(ctx, L);
+  if (kind == 0) {
+    ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, (double*)f_dev, 0, 3, false));
+    k_load_nodal<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(g, (const double*)f_dev, b_dev);
+    return launched(ctx);
+  }
+  if (kind == 1) {
+    if (!table || nftab < 1 || nftab > 256) return STK_EINVAL;
+    double* dt;
+    CK(cudaMallocAsync(&dt, sizeof(double) * 3 * nftab, ctx->stream));
+    CK(cudaMemcpyAsync(dt, table, sizeof(double) * 3 * nftab, cudaMemcpyHostToDevice, ctx->stream));
+    k_load_elem<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(g, (const uint8_t*)f_dev, dt, b_dev);
+    stk_status s = launched(ctx);
+    CK(cudaFreeAsync(dt, ctx->stream));
+    return s;
+  }
+  return STK_EINVAL;
+}
+
+stk_status stk_apply(stk_ctx* ctx, int32_t level, uint32_t blocks, const double* x, double* y) {
+  ST(check(ctx, 2));
+  ST(check_level(ctx, level));
+  return op_apply(ctx, level, blocks & BLK_ALL, x, y);
+}
+
+stk_status stk_norms(stk_ctx* ctx, int32_t level, const double* x, double* out) {
+  ST(check(ctx, 2));
+  ST(check_level(ctx, level));
+  ST(op_partials(ctx, level, x, 0));
+  CK(cudaMemcpyAsync(ctx->hsums, ctx->sums, sizeof(double) * 6, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int q = 0; q < 4; ++q) out[q] = ctx->hsums[q];
+  out[4] = out[0] + out[1] + out[2] + out[3];
+  return STK_OK;
+}
+
+stk_status stk_residual(stk_ctx* ctx, int32_t level, const double* x, const double* b, double* r,
+                        double* norms) {
+  ST(check(ctx, 2));
+  ST(check_level(ctx, level));
+  ST(op_residual(ctx, level, x, b, r));
+  if (norms) return stk_norms(ctx, level, r, norms);
+  return STK_OK;
+}
+
+stk_status stk_smooth(stk_ctx* ctx, int32_t level, double* x, const double* b, int32_t steps) {
+  ST(check(ctx, 2));
+  ST(check_level(ctx, level));
+  if (level == ctx->nlev - 1 && ctx->nlev > 1) { /* allowed: smoothing on the coarsest grid */ }
+  for (int s = 0; s < steps; ++s) ST(op_uzawa(ctx, level, x, b));
+  return STK_OK;
+}
+
+stk_status stk_restrict(stk_ctx* ctx, int32_t fine_level, const double* r_f, double* b_c) {
+  ST(check(ctx, 2));
+  if (fine_level < 0 || fine_level >= ctx->nlev - 1) return STK_EINVAL;
+  return op_restrict(ctx, fine_level, r_f, b_c);
+}
+
+stk_status stk_prolong_add(stk_ctx* ctx, int32_t coarse_level, const double* x_c, double* x_f) {
+  ST(check(ctx, 2));
+  if (coarse_level < 1 || coarse_level >= ctx->nlev) return STK_EINVAL;
+  return op_prolong_add(ctx, coarse_level, x_c, x_f);
+}
+
+stk_status stk_vcycle(stk_ctx* ctx, const double* b, double* x) {
+  ST(check(ctx, 2));
+  return op_vcycle(ctx, 0, b, x);
+}
+
+stk_status stk_gauge(stk_ctx* ctx, int32_t level, double* x) {
+  ST(check(ctx, 2));
+  ST(check_level(ctx, level));
+  return op_gauge(ctx, level, x);
+}
+
+stk_status stk_solve(stk_ctx* ctx, const double* b, double* x, double rtol, int32_t max_cycles,
+                     stk_report* rep) {
+  ST(check(ctx, 2));
+  Level& L = ctx->lev[0];
+  stk_report local{};
+  stk_report* R = rep ? rep : &local;
+  memset(R, 0, sizeof(*R));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, ctx->stream));
+  double nb[5];
+  ST(stk_norms(ctx, 0, b, nb));
+  const double bnorm = std::sqrt(nb[4]);
+  double nr[5];
+  ST(stk_residual(ctx, 0, x, b, L.r, nr));
+  double rel = bnorm > 0 ? std::sqrt(nr[4]) / bnorm : 0.0;
+  R->res_hist[0] = rel;
+  int cyc = 0;
+  stk_status st = STK_OK;
+  while (rel > rtol && cyc < max_cycles) {
+    ST(op_vcycle(ctx, 0, b, x));
+    ST(stk_residual(ctx, 0, x, b, L.r, nr));
+    ++cyc;
+    rel = bnorm > 0 ? std::sqrt(nr[4]) / bnorm : 0.0;
+    if (cyc < 256) R->res_hist[cyc] = rel;
+    if (!std::isfinite(rel)) {
+      R->nan_seen = 1;
+      break;
+    }
+  }
+  ST(op_gauge(ctx, 0, x));
+  CK(cudaEventRecord(e1, ctx->stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  R->cycles = cyc;
+  R->rel_res = rel;
+  R->t_total_s = ms * 1e-3;
+  const int m = std::min(cyc, 255);
+  const int first = std::max(1, m - 5);
+  R->rho = (m >= 1 && R->res_hist[first - 1] > 0)
+               ? std::pow(R->res_hist[m] / R->res_hist[first - 1], 1.0 / (m - first + 1))
+               : 0.0;
+  if (!(rel <= rtol)) st = STK_ENOCONV;
+  return st;
+}
+
+stk_status stk_set_kernel_mode(stk_ctx* ctx, int32_t mode) {
+  if (!ctx || (mode != 0 && mode != 1)) return STK_EINVAL;
+  ctx->kernel_mode = mode;
+  return STK_OK;
+}
+
+int64_t stk_launch_count(const stk_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* stk_last_error(const stk_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+stk_status stk_destroy(stk_ctx* ctx) {
+  if (!ctx) return STK_EINVAL;
+  for (auto& L : ctx->lev) {
+    cudaFree(L.cls);
+    cudaFree(L.code);
+    cudaFree(L.x);
+    cudaFree(L.b);
+    cudaFree(L.r);
+  }
+  cudaFree(ctx->cdofs);
+  cudaFree(ctx->cK);
+  cudaFree(ctx->cG);
+  cudaFree(ctx->cstatus);
+  cudaFree(ctx->part);
+  cudaFree(ctx->sums);
+  cudaFreeHost(ctx->hsums);
+  ctx->comm.destroy();
+  delete ctx;
+  return STK_OK;
+}
+
+}  // extern "C"

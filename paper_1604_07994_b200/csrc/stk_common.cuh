@@ -1,0 +1,187 @@
+// Common device definitions of the B200 Stokes library (sm_100a, fp64).
+//
+// Grid: unit cube, n^3 cubes, each split into the 6 Kuhn tetrahedra
+//   t <-> sigma in {(x,y,z),(x,z,y),(y,x,z),(y,z,x),(z,x,y),(z,y,x)}
+//   a0 = c, a1 = a0 + h e_s1, a2 = a1 + h e_s2, a3 = c + h(1,1,1)
+// which is the six-tetrahedra split of P:720; uniform (Bey) refinement of this
+// mesh is the same Kuhn grid at h/2, so every level is structured.
+//
+// Layout of a level vector (z-slab of this rank): 4 fields (u1,u2,u3,p),
+//   f*fs + (k - z0 + 1)*py + j*px + i,   planes z0-1 and z0+nzl are halos.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace stk {
+
+enum { FORM_MOD = 0, FORM_SYM = 1, FORM_GRAD = 2 };
+enum { BLK_A = 1, BLK_BT = 2, BLK_B = 4, BLK_C = 8, BLK_ALL = 15 };
+constexpr uint8_t CODE_IRREGULAR = 0xFF;
+
+// per-class viscosity mu_k and 1/mu_k
+__constant__ double c_mu[256];
+__constant__ double c_inv_mu[256];
+// Kuhn permutations
+__constant__ int8_t c_perm[6][3];
+// local index (0..3) of cube corner `corner` (bit0 x, bit1 y, bit2 z) in tet t, or -1
+__constant__ int8_t c_corner_m[8][6];
+// Bey children of a coarse tet T: fine cube offset (bits x|y<<1|z<<2) and fine type
+__constant__ int8_t c_child_off[6][8];
+__constant__ int8_t c_child_t[6][8];
+
+struct DGrid {
+  int n;            // intervals of this level
+  int z0, nzl;      // owned vertex planes [z0, z0+nzl)
+  int cz0;          // first stored cube layer
+  int64_t px, py, fs;
+  double h;
+  double delta;     // stabilisation constant
+  unsigned dirmask; // bit f set: face f is homogeneous Dirichlet
+  const uint8_t* cls;   // element classes [cz - cz0][cj][ci][t]
+  const uint8_t* code;  // per-vertex code (plane layout of one field)
+};
+
+__device__ __forceinline__ int64_t vidx(const DGrid& g, int i, int j, int k) {
+  return (int64_t)(k - g.z0 + 1) * g.py + (int64_t)j * g.px + i;
+}
+
+__device__ __forceinline__ bool is_dirichlet(const DGrid& g, int i, int j, int k) {
+  const unsigned m = g.dirmask;
+  return ((m & 1u) && i == 0) || ((m & 2u) && i == g.n) || ((m & 4u) && j == 0) ||
+         ((m & 8u) && j == g.n) || ((m & 16u) && k == 0) || ((m & 32u) && k == g.n);
+}
+
+__device__ __forceinline__ uint8_t elem_class(const DGrid& g, int ci, int cj, int ck, int t) {
+  return g.cls[((((int64_t)(ck - g.cz0)) * g.n + cj) * g.n + ci) * 6 + t];
+}
+
+// Fetch functor: 4-field vector in the level layout, velocity masked at Dirichlet.
+struct FetchVec {
+  const double* __restrict__ u;  // base of fields 0..2 (stride fs)
+  const double* __restrict__ p;  // pressure field base
+  __device__ __forceinline__ double operator()(const DGrid& g, int i, int j, int k, int f) const {
+    const int64_t o = vidx(g, i, j, k);
+    if (f == 3) return p[o];
+    if (is_dirichlet(g, i, j, k)) return 0.0;
+    return u[f * g.fs + o];
+  }
+};
+
+// Generic row of K = [[A, B^T], [B, -C]] at owned vertex (i,j,k), by the
+// element loop over its 24 incident tetrahedra (exact P1 integration):
+//   (A u)_{i,a} = sum_T mu_T |T| [(G + G^T - tr(G) I) g_m]_a      (mod)
+//                 sum_T mu_T |T| [(G + G^T) g_m]_a               (sym)
+//                 sum_T mu_T |T| [G g_m]_a                       (grad)
+//   (B^T p)_{i,a} = -sum_T |T|/4 g_m[a] sum_{q in T} p_q
+//   (B u)_i       = -sum_T |T|/4 tr(G)
+//   (C p)_i       =  sum_T delta h^2/mu_T |T| g_m . grad p        (DESIGN R1)
+// G = grad u on T from the Kuhn path differences, g_m = grad lambda_m.
+// Also returns the diagonals of A (per component) and C (for Gauss-Seidel).
+template <int FORM, class F>
+__device__ __forceinline__ void row_generic(const DGrid& g, int i, int j, int k, const F& fx,
+                                            unsigned blocks, double y[4], double dA[3],
+                                            double& dC) {
+  const double h = g.h, hinv = 1.0 / h;
+  const double vol = h * h * h / 6.0, vq = 0.25 * vol;
+  const double cstab = g.delta * h * h * vol;
+  y[0] = y[1] = y[2] = y[3] = 0.0;
+  dA[0] = dA[1] = dA[2] = 0.0;
+  dC = 0.0;
+  for (int dz = -1; dz <= 0; ++dz) {
+    const int ck = k + dz;
+    if (ck < 0 || ck >= g.n) continue;
+    for (int dy = -1; dy <= 0; ++dy) {
+      const int cj = j + dy;
+      if (cj < 0 || cj >= g.n) continue;
+      for (int dx = -1; dx <= 0; ++dx) {
+        const int ci = i + dx;
+        if (ci < 0 || ci >= g.n) continue;
+        const int corner = (-dx) | ((-dy) << 1) | ((-dz) << 2);
+        for (int t = 0; t < 6; ++t) {
+          const int m = c_corner_m[corner][t];
+          if (m < 0) continue;
+          const int s1 = c_perm[t][0], s2 = c_perm[t][1], s3 = c_perm[t][2];
+          int v[4][3];
+          v[0][0] = ci; v[0][1] = cj; v[0][2] = ck;
+          v[1][0] = ci; v[1][1] = cj; v[1][2] = ck; v[1][s1] += 1;
+          v[2][0] = v[1][0]; v[2][1] = v[1][1]; v[2][2] = v[1][2]; v[2][s2] += 1;
+          v[3][0] = ci + 1; v[3][1] = cj + 1; v[3][2] = ck + 1;
+          double val[4][4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int f = 0; f < 4; ++f) val[q][f] = fx(g, v[q][0], v[q][1], v[q][2], f);
+          double G[3][3], gp[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            G[a][s1] = (val[1][a] - val[0][a]) * hinv;
+            G[a][s2] = (val[2][a] - val[1][a]) * hinv;
+            G[a][s3] = (val[3][a] - val[2][a]) * hinv;
+          }
+          gp[s1] = (val[1][3] - val[0][3]) * hinv;
+          gp[s2] = (val[2][3] - val[1][3]) * hinv;
+          gp[s3] = (val[3][3] - val[2][3]) * hinv;
+          double gm[3] = {0.0, 0.0, 0.0};
+          if (m == 0) {
+            gm[s1] = -hinv;
+          } else if (m == 1) {
+            gm[s1] = hinv; gm[s2] = -hinv;
+          } else if (m == 2) {
+            gm[s2] = hinv; gm[s3] = -hinv;
+          } else {
+            gm[s3] = hinv;
+          }
+          const uint8_t cl = elem_class(g, ci, cj, ck, t);
+          const double mu = c_mu[cl], imu = c_inv_mu[cl];
+          const double gg = gm[0] * gm[0] + gm[1] * gm[1] + gm[2] * gm[2];
+          const double tr = G[0][0] + G[1][1] + G[2][2];
+          if (blocks & BLK_A) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              double s = G[a][0] * gm[0] + G[a][1] * gm[1] + G[a][2] * gm[2];
+              if (FORM != FORM_GRAD) s += G[0][a] * gm[0] + G[1][a] * gm[1] + G[2][a] * gm[2];
+              if (FORM == FORM_MOD) s -= tr * gm[a];
+              y[a] += mu * vol * s;
+            }
+          }
+          if (blocks & BLK_BT) {
+            const double ps = val[0][3] + val[1][3] + val[2][3] + val[3][3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) y[a] -= vq * gm[a] * ps;
+          }
+          if (blocks & BLK_B) y[3] -= vq * tr;
+          if (blocks & BLK_C) y[3] -= cstab * imu * (gm[0] * gp[0] + gm[1] * gp[1] + gm[2] * gp[2]);
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            dA[a] += mu * vol * (gg + (FORM == FORM_SYM ? gm[a] * gm[a] : 0.0));
+          dC += cstab * imu * gg;
+        }
+      }
+    }
+  }
+  if (is_dirichlet(g, i, j, k)) y[0] = y[1] = y[2] = 0.0;
+}
+
+// w_j = int phi_j / mu = sum_{T ni j} |T| / (4 mu_T)   (gauge weight)
+__device__ __forceinline__ double gauge_weight(const DGrid& g, int i, int j, int k) {
+  const double vq = 0.25 * g.h * g.h * g.h / 6.0;
+  double w = 0.0;
+  for (int dz = -1; dz <= 0; ++dz) {
+    const int ck = k + dz;
+    if (ck < 0 || ck >= g.n) continue;
+    for (int dy = -1; dy <= 0; ++dy) {
+      const int cj = j + dy;
+      if (cj < 0 || cj >= g.n) continue;
+      for (int dx = -1; dx <= 0; ++dx) {
+        const int ci = i + dx;
+        if (ci < 0 || ci >= g.n) continue;
+        const int corner = (-dx) | ((-dy) << 1) | ((-dz) << 2);
+        for (int t = 0; t < 6; ++t)
+          if (c_corner_m[corner][t] >= 0) w += vq * c_inv_mu[elem_class(g, ci, cj, ck, t)];
+      }
+    }
+  }
+  return w;
+}
+
+}  // namespace stk

@@ -141,8 +141,18 @@ def _classes_block(cfg: Config, k0: int, k1: int):
     elif name == "cfg4":
         c, r = _spheres(cfg.seed)
         inside = np.zeros(x.shape, dtype=bool)
+        n = cfg.n
         for s in range(len(r)):
-            inside |= (x - c[s, 0]) ** 2 + (y - c[s, 1]) ** 2 + (z - c[s, 2]) ** 2 < r[s] ** 2
+            # only cubes whose index box can hold a centroid inside sphere s
+            lo = np.floor((c[s] - r[s]) * n).astype(int) - 1
+            hi = np.ceil((c[s] + r[s]) * n).astype(int) + 1
+            kk0, kk1 = max(lo[2], k0), min(hi[2], k1)
+            if kk0 >= kk1:
+                continue
+            sl = (slice(kk0 - k0, kk1 - k0), slice(max(lo[1], 0), min(hi[1], n)),
+                  slice(max(lo[0], 0), min(hi[0], n)))
+            xs, ys, zs = x[sl], y[sl], z[sl]
+            inside[sl] |= (xs - c[s, 0]) ** 2 + (ys - c[s, 1]) ** 2 + (zs - c[s, 2]) ** 2 < r[s] ** 2
         mu_cls = np.where(inside, 1, 0)
         f_cls = np.zeros_like(mu_cls)
     elif name == "cfg5":

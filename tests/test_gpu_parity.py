@@ -1,0 +1,216 @@
+"""GPU path (C ABI via the binding) vs the oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): one operator apply within 1e-12
+relative per field; MG pieces within 1e-12 (transfers 1e-14); a converged
+solve within 1e-8 relative per field after the pressure gauge.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import capi, fem, mg
+from gpu_util import make_ctx, per_field_rel, rhs_oracle_and_gpu
+
+pytestmark = pytest.mark.gpu
+
+TOL_APPLY = 1e-12
+
+
+def _oracle_problem(cfg, cls, form):
+    return fem.problem_from_classes(cfg.n, cls, cfg.class_mu, cfg.faces, form)
+
+
+@pytest.mark.parametrize("cfgname,n,form,mode", [
+    ("cfg1", 16, "mod", 0), ("cfg1", 16, "mod", 1),
+    ("cfg2", 32, "mod", 1), ("cfg2", 32, "sym", 1), ("cfg2", 32, "grad", 1),
+    ("cfg3", 32, "mod", 1), ("cfg5", 32, "mod", 1),
+])
+def test_apply_small_vs_assembled_oracle(cfgname, n, form, mode):
+    ctx, cfg, cls, _ = make_ctx(cfgname, n, form, kernel_mode=mode)
+    pr = _oracle_problem(cfg, cls, form)
+    x = synth.apply_input(cfg)
+    y_o = pr.apply(x.reshape(-1)).reshape(4, -1)
+    y_g = ctx.export(ctx.apply(ctx.import_(x)))
+    err, errs = per_field_rel(y_g, y_o)
+    assert err <= TOL_APPLY, errs
+
+
+@pytest.mark.parametrize("blocks", [1, 2, 4, 8, 5, 10])
+def test_apply_blocks(blocks):
+    ctx, cfg, cls, _ = make_ctx("cfg2", 16, "mod")
+    pr = _oracle_problem(cfg, cls, "mod")
+    V = pr.V
+    x = synth.apply_input(cfg).reshape(-1)
+    xf = np.where(pr.free, x, 0.0)
+    u, p = xf[:3 * V], xf[3 * V:]
+    yu = np.zeros(3 * V)
+    yp = np.zeros(V)
+    if blocks & 1:
+        yu += pr.A @ u
+    if blocks & 2:
+        yu += pr.B.T @ p
+    if blocks & 4:
+        yp += pr.B @ u
+    if blocks & 8:
+        yp -= pr.C @ p
+    y_o = np.where(pr.free, np.concatenate([yu, yp]), 0.0).reshape(4, -1)
+    y_g = ctx.export(ctx.apply(ctx.import_(x.reshape(4, -1)), blocks=blocks))
+    for f in range(4):
+        nb = np.linalg.norm(y_o[f])
+        if nb == 0:
+            assert np.abs(y_g[f]).max() == 0.0
+        else:
+            assert np.linalg.norm(y_g[f] - y_o[f]) <= TOL_APPLY * nb
+
+
+@pytest.mark.parametrize("cfgname,n", [("cfg4", 64), ("cfg4", 128), ("cfg3", 128), ("cfg5", 128),
+                                       ("cfg2", 128)])
+def test_apply_full_grid_vs_c_oracle(cfgname, n):
+    ctx, cfg, cls, _ = make_ctx(cfgname, n, "mod")
+    x = synth.apply_input(cfg)
+    y_o = capi.apply_slab(n, "mod", 1 / 12, cfg.faces, cls, cfg.class_mu, x).reshape(4, -1)
+    y_g = ctx.export(ctx.apply(ctx.import_(x)))
+    err, errs = per_field_rel(y_g, y_o)
+    assert err <= TOL_APPLY, errs
+
+
+@pytest.mark.parametrize("cfgname,n", [("cfg4", 512), ("cfg3", 256), ("cfg2", 128)])
+def test_apply_bench_size_sampled_rows(cfgname, n):
+    """Full BASELINE size, same launch configuration as bench.py: rows at sampled
+    vertices (random + every irregular class of row: boundary faces, edges, corners,
+    interface) recomputed one by one by the C oracle."""
+    ctx, cfg, cls, _ = make_ctx(cfgname, n, "mod")
+    x = synth.apply_input(cfg)
+    y_g = ctx.export(ctx.apply(ctx.import_(x)))
+    rng = np.random.default_rng(11)
+    V = cfg.vertices
+    N1 = n + 1
+    picks = [rng.integers(0, V, 20000)]
+    # boundary faces / edges / corners
+    for (i, j, k) in [(0, 5, 7), (n, 3, 9), (4, 0, 6), (6, n, 2), (2, 3, 0), (7, 5, n),
+                      (0, 0, 5), (n, n, 5), (0, 0, 0), (n, n, n), (0, n, n)]:
+        picks.append(np.array([i + N1 * (j + N1 * k)]))
+    # interface rows: vertices whose star holds two classes
+    c4 = cls.reshape(n, n, n, 6)
+    jump = np.flatnonzero((c4.min(axis=3) != c4.max(axis=3)).reshape(-1))[:5000]
+    ci, cj, ck = jump % n, (jump // n) % n, jump // (n * n)
+    picks.append(ci + N1 * (cj + N1 * ck))
+    verts = np.unique(np.concatenate(picks))
+    rows = capi.apply_rows(n, "mod", 1 / 12, cfg.faces, cls, cfg.class_mu, x, verts)
+    got = y_g[:, verts].T
+    scale = np.abs(rows).max(axis=0)
+    assert np.all(np.abs(got - rows) <= 1e-12 * scale[None, :]), np.abs(got - rows).max(axis=0) / scale
+
+
+@pytest.mark.parametrize("cfgname,n", [("cfg1", 16), ("cfg3", 16), ("cfg5", 16)])
+def test_load_vector(cfgname, n):
+    ctx, cfg, cls, fcls = make_ctx(cfgname, n, "mod")
+    pr = _oracle_problem(cfg, cls, "mod")
+    b_o, b_g = rhs_oracle_and_gpu(ctx, cfg, cls, fcls, pr)
+    y = ctx.export(b_g)
+    assert np.abs(y - b_o.reshape(4, -1)).max() <= 1e-13 * np.abs(b_o).max()
+
+
+def test_classification_and_coarse_classes():
+    import paper_1604_07994_b200 as stk
+    n = 64
+    ctx, cfg, cls, _ = make_ctx("cfg4", n, "mod")
+    # irregular = boundary vertex or a star with more than one viscosity
+    c4 = cls.reshape(n, n, n, 6)
+    N1 = n + 1
+    star_min = np.full((N1, N1, N1), 255)
+    star_max = np.full((N1, N1, N1), -1)
+    for dz in (0, 1):
+        for dy in (0, 1):
+            for dx in (0, 1):
+                sl = (slice(dz, dz + n), slice(dy, dy + n), slice(dx, dx + n))
+                star_min[sl] = np.minimum(star_min[sl], c4.min(axis=3))
+                star_max[sl] = np.maximum(star_max[sl], c4.max(axis=3))
+    bnd = np.zeros((N1,) * 3, bool)
+    bnd[0], bnd[-1], bnd[:, 0], bnd[:, -1], bnd[:, :, 0], bnd[:, :, -1] = [True] * 6
+    irr = bnd | (star_min != star_max)
+    assert ctx.layout(0).n_irregular == int(irr.sum())
+    # coarse level classes == oracle majority rule, level by level (through the irregular counts)
+    h = mg.Hierarchy(n, cls, cfg.class_mu, cfg.faces)
+    for l, lev in enumerate(h.levels):
+        m = lev.n
+        c = lev.cls.reshape(m, m, m, 6)
+        M1 = m + 1
+        smin = np.full((M1,) * 3, 255)
+        smax = np.full((M1,) * 3, -1)
+        for dz in (0, 1):
+            for dy in (0, 1):
+                for dx in (0, 1):
+                    sl = (slice(dz, dz + m), slice(dy, dy + m), slice(dx, dx + m))
+                    smin[sl] = np.minimum(smin[sl], c.min(axis=3))
+                    smax[sl] = np.maximum(smax[sl], c.max(axis=3))
+        b = np.zeros((M1,) * 3, bool)
+        b[0], b[-1], b[:, 0], b[:, -1], b[:, :, 0], b[:, :, -1] = [True] * 6
+        assert ctx.layout(l).n_irregular == int((b | (smin != smax)).sum())
+
+
+@pytest.mark.parametrize("cfgname,form,mode", [("cfg1", "mod", 0), ("cfg2", "mod", 1),
+                                               ("cfg2", "sym", 1), ("cfg3", "grad", 1)])
+def test_uzawa_step_and_vcycle(cfgname, form, mode):
+    n = 16 if mode == 0 else 32
+    nc = 4 if form == "sym" else 2
+    ctx, cfg, cls, fcls = make_ctx(cfgname, n, form, kernel_mode=mode, ncolors_u=nc)
+    h = mg.Hierarchy(n, cls, cfg.class_mu, cfg.faces, form=form, ncolors_u=nc)
+    pr = h.levels[0].prob
+    rng = np.random.default_rng(3)
+    x = np.where(pr.free, rng.uniform(-1, 1, 4 * pr.V), 0.0)
+    b = np.where(pr.free, rng.uniform(-1, 1, 4 * pr.V), 0.0) * 1e-3
+    # one smoothing step
+    xs_o = h.uzawa(h.levels[0], x, b)
+    xg = ctx.import_(x.reshape(4, -1))
+    bg = ctx.import_(b.reshape(4, -1))
+    ctx.smooth(xg, bg, 1)
+    err, errs = per_field_rel(ctx.export(xg), xs_o)
+    assert err <= 1e-12, errs
+    # one V-cycle from the smoothed iterate
+    xv_o = h.vcycle(b, xs_o)
+    ctx.vcycle(bg, xg)
+    err, errs = per_field_rel(ctx.export(xg), xv_o)
+    assert err <= 1e-10, errs
+
+
+def test_transfers():
+    n = 32
+    ctx, cfg, cls, _ = make_ctx("cfg2", n, "mod")
+    P = mg.prolongation(n // 2)
+    rng = np.random.default_rng(5)
+    pf = fem.Problem(n, np.ones(6 * n ** 3), cfg.faces)
+    pc = fem.Problem(n // 2, np.ones(6 * (n // 2) ** 3), cfg.faces)
+    r = np.where(pf.free, rng.standard_normal(4 * pf.V), 0.0).reshape(4, -1)
+    bc_o = np.where(pc.free, np.concatenate([P.T @ r[f] for f in range(4)]), 0.0).reshape(4, -1)
+    bc_g = ctx.export(ctx.restrict(ctx.import_(r)), level=1)
+    assert np.abs(bc_g - bc_o).max() <= 1e-14 * np.abs(bc_o).max()
+    xc = np.where(pc.free, rng.standard_normal(4 * pc.V), 0.0).reshape(4, -1)
+    xf = np.where(pf.free, rng.standard_normal(4 * pf.V), 0.0).reshape(4, -1)
+    xf_o = np.where(pf.free, (xf + np.stack([P @ xc[f] for f in range(4)])).reshape(-1), 0.0)
+    xfv = ctx.import_(xf)
+    ctx.prolong_add(ctx.import_(xc, level=1), xfv, coarse_level=1)
+    assert np.abs(ctx.export(xfv).reshape(-1) - xf_o).max() <= 1e-14 * np.abs(xf_o).max()
+
+
+@pytest.mark.parametrize("cfgname,n,form", [("cfg1", 16, "mod"), ("cfg2", 16, "mod"),
+                                            ("cfg3", 16, "mod"), ("cfg5", 16, "mod"),
+                                            ("cfg2", 16, "sym"), ("cfg2", 32, "mod")])
+def test_solve_matches_direct_solution(cfgname, n, form):
+    nc = 4 if form == "sym" else 2
+    ctx, cfg, cls, fcls = make_ctx(cfgname, n, form, ncolors_u=nc)
+    pr = _oracle_problem(cfg, cls, form)
+    b_o, b_g = rhs_oracle_and_gpu(ctx, cfg, cls, fcls, pr)
+    x_d = pr.solve_direct(b_o)
+    xg, rep = ctx.solve(b_g, rtol=1e-12, max_cycles=100)
+    assert rep.rel_res <= 1e-12
+    err, errs = per_field_rel(ctx.export(xg), x_d.reshape(4, -1))
+    assert err <= 1e-8, errs
+
+
+def test_solve_cfg1_rate():
+    ctx, cfg, cls, fcls = make_ctx("cfg1", 16, "mod")
+    pr = _oracle_problem(cfg, cls, "mod")
+    b_o, b_g = rhs_oracle_and_gpu(ctx, cfg, cls, fcls, pr)
+    xg, rep = ctx.solve(b_g, rtol=1e-8)
+    assert rep.rel_res <= 1e-8 and rep.cycles <= 30 and 0 < rep.rho < 0.6
