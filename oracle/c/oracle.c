@@ -102,7 +102,7 @@ static inline int is_dirichlet(int n, const int32_t* faces, int i, int j, int k)
  * of local vertex m are added only if row_ok[m].  x, y indexed with plane offset. */
 static void element_apply(int n, int form, double delta, const int32_t* faces, const elem_t* e,
                           double mu, int ci, int cj, int ck, const double* x, double* y,
-                          int64_t V, int64_t kbase_x, int64_t kbase_y, int kv0, int kv1) {
+                          int64_t V, unsigned blocks, int kv0, int kv1) {
   const int64_t N1 = n + 1;
   double xl[16], yl[16];
   int64_t vid[4];
@@ -112,27 +112,27 @@ static void element_apply(int n, int form, double delta, const int32_t* faces, c
     vk[m] = k;
     dir[m] = is_dirichlet(n, faces, i, j, k);
     vid[m] = i + N1 * (j + N1 * (int64_t)k);
-    for (int a = 0; a < 3; ++a) xl[a * 4 + m] = dir[m] ? 0.0 : x[a * V + vid[m] - kbase_x];
-    xl[12 + m] = x[3 * V + vid[m] - kbase_x];
+    for (int a = 0; a < 3; ++a) xl[a * 4 + m] = dir[m] ? 0.0 : x[a * V + vid[m]];
+    xl[12 + m] = x[3 * V + vid[m]];
   }
   const double (*A)[12] = e->A[form];
   for (int r = 0; r < 12; ++r) {
     double s = 0.0;
-    for (int c = 0; c < 12; ++c) s += mu * A[r][c] * xl[c];
-    for (int c = 0; c < 4; ++c) s += e->B[c][r] * xl[12 + c];
+    if (blocks & 1) for (int c = 0; c < 12; ++c) s += mu * A[r][c] * xl[c];
+    if (blocks & 2) for (int c = 0; c < 4; ++c) s += e->B[c][r] * xl[12 + c];
     yl[r] = s;
   }
   for (int r = 0; r < 4; ++r) {
     double s = 0.0;
-    for (int c = 0; c < 12; ++c) s += e->B[r][c] * xl[c];
-    for (int c = 0; c < 4; ++c) s -= (delta / mu) * e->C[r][c] * xl[12 + c];
+    if (blocks & 4) for (int c = 0; c < 12; ++c) s += e->B[r][c] * xl[c];
+    if (blocks & 8) for (int c = 0; c < 4; ++c) s -= (delta / mu) * e->C[r][c] * xl[12 + c];
     yl[12 + r] = s;
   }
   for (int m = 0; m < 4; ++m) {
     if (vk[m] < kv0 || vk[m] >= kv1) continue;
     for (int a = 0; a < 3; ++a)
-      if (!dir[m]) y[a * V + vid[m] - kbase_y] += yl[a * 4 + m];
-    y[3 * V + vid[m] - kbase_y] += yl[12 + m];
+      if (!dir[m]) y[a * V + vid[m]] += yl[a * 4 + m];
+    y[3 * V + vid[m]] += yl[12 + m];
   }
 }
 
@@ -140,7 +140,8 @@ static void element_apply(int n, int form, double delta, const int32_t* faces, c
  * x holds the full grid (4 x V); y holds the full grid too (rows outside
  * [kv0,kv1) untouched).  Returns 0. */
 int ora_apply_slab(int n, int form, double delta, const int32_t* faces, const uint8_t* cls,
-                   const double* class_mu, const double* x, double* y, int kv0, int kv1) {
+                   const double* class_mu, const double* x, double* y, int kv0, int kv1,
+                   unsigned blocks) {
   const int64_t N1 = n + 1, V = N1 * N1 * N1;
   elem_t E[6];
   build_elements(1.0 / n, E);
@@ -156,7 +157,7 @@ int ora_apply_slab(int n, int form, double delta, const int32_t* faces, const ui
           for (int t = 0; t < 6; ++t) {
             int64_t eid = 6 * (ci + (int64_t)n * (cj + (int64_t)n * ck)) + t;
             element_apply(n, form, delta, faces, &E[t], class_mu[cls[eid]], ci, cj, ck, x, y, V,
-                          0, 0, kv0, kv1);
+                          blocks, kv0, kv1);
           }
     }
   }
@@ -218,6 +219,30 @@ int ora_apply_rows(int n, int form, double delta, const int32_t* faces, const ui
     for (int a = 0; a < 3; ++a) out[4 * s + a] = d ? 0.0 : acc[a];
     out[4 * s + 3] = acc[3];
   }
+  return 0;
+}
+
+/* diagonals of A (3 x V, per component) and C (V) by the element loop */
+int ora_diag(int n, int form, double delta, const int32_t* faces, const uint8_t* cls,
+             const double* class_mu, double* dA, double* dC) {
+  const int64_t N1 = n + 1, V = N1 * N1 * N1;
+  elem_t E[6];
+  build_elements(1.0 / n, E);
+  memset(dA, 0, sizeof(double) * 3 * V);
+  memset(dC, 0, sizeof(double) * V);
+  for (int ck = 0; ck < n; ++ck)
+    for (int cj = 0; cj < n; ++cj)
+      for (int ci = 0; ci < n; ++ci)
+        for (int t = 0; t < 6; ++t) {
+          const elem_t* e = &E[t];
+          double mu = class_mu[cls[6 * (ci + (int64_t)n * (cj + (int64_t)n * ck)) + t]];
+          for (int m = 0; m < 4; ++m) {
+            int64_t v = (ci + e->off[m][0]) + N1 * ((cj + e->off[m][1]) + N1 * (int64_t)(ck + e->off[m][2]));
+            for (int a = 0; a < 3; ++a) dA[a * V + v] += mu * e->A[form][a * 4 + m][a * 4 + m];
+            dC[v] += (delta / mu) * e->C[m][m];
+          }
+        }
+  (void)faces;
   return 0;
 }
 

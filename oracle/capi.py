@@ -27,7 +27,8 @@ def lib():
         L = ctypes.CDLL(LIB)
         P = ctypes.c_void_p
         L.ora_apply_slab.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, P, P, P, P, P,
-                                     ctypes.c_int, ctypes.c_int]
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_uint]
+        L.ora_diag.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, P, P, P, P, P]
         L.ora_apply_rows.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, P, P, P, P, P,
                                      ctypes.c_int64, P]
         L.ora_num_threads.restype = ctypes.c_int
@@ -39,7 +40,7 @@ def _p(a):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
-def apply_slab(n, form, delta, faces, cls, class_mu, x, kv0=0, kv1=None, y=None):
+def apply_slab(n, form, delta, faces, cls, class_mu, x, kv0=0, kv1=None, y=None, blocks=15):
     """y = K x for the rows of vertex planes [kv0, kv1); x, y field-major (4, V)."""
     kv1 = n + 1 if kv1 is None else kv1
     V = (n + 1) ** 3
@@ -48,8 +49,21 @@ def apply_slab(n, form, delta, faces, cls, class_mu, x, kv0=0, kv1=None, y=None)
     f = np.ascontiguousarray(faces, dtype=np.int32)
     c = np.ascontiguousarray(cls, dtype=np.uint8)
     m = np.ascontiguousarray(class_mu, dtype=np.float64)
-    lib().ora_apply_slab(n, FORM_ID[form], float(delta), _p(f), _p(c), _p(m), _p(x), _p(y), kv0, kv1)
+    lib().ora_apply_slab(n, FORM_ID[form], float(delta), _p(f), _p(c), _p(m), _p(x), _p(y), kv0, kv1,
+                         blocks)
     return y
+
+
+def diagonals(n, form, delta, faces, cls, class_mu):
+    """(diag A (3V,), diag C (V,)) by the element loop."""
+    V = (n + 1) ** 3
+    dA = np.zeros(3 * V)
+    dC = np.zeros(V)
+    f = np.ascontiguousarray(faces, dtype=np.int32)
+    c = np.ascontiguousarray(cls, dtype=np.uint8)
+    m = np.ascontiguousarray(class_mu, dtype=np.float64)
+    lib().ora_diag(n, FORM_ID[form], float(delta), _p(f), _p(c), _p(m), _p(dA), _p(dC))
+    return dA, dC
 
 
 def apply_rows(n, form, delta, faces, cls, class_mu, x, verts):

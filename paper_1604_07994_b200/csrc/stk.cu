@@ -160,9 +160,6 @@ void host_tables(int8_t perm[6][3], int8_t corner[8][6], int8_t choff[6][8], int
   }
 }
 
-template <class K1, class K2, class K3>
-void pick_form(int form, K1 k_mod, K2 k_sym, K3 k_grad);
-
 // ---- level operations ------------------------------------------------------
 
 bool use_tiled(const stk_ctx* ctx, const Level& L) {
@@ -248,7 +245,7 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
   ST(launched(ctx));
   ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, tmp, 3, 1, L.replicated));
   if (tiled) {
-    ST(launch_p_pass2_tiled(g, T, p, ctx->cfg.omega, ctx->stream) ? STK_OK : STK_EUNSUP);
+    ST(launch_p_pass2_tiled(ctx->cfg.form, g, T, p, ctx->cfg.omega, ctx->stream) ? STK_OK : STK_EUNSUP);
   } else {
     k_p_pass2_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, T, p, ctx->cfg.omega);
   }
@@ -322,12 +319,32 @@ stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x) {
   return STK_OK;
 }
 
+const stk_ctx* g_active = nullptr;  // context whose viscosity table is in constant memory
+
+// The per-class viscosity table lives in __constant__ memory (broadcast reads);
+// with several contexts in one process, re-upload it when the caller switches.
+stk_status activate(stk_ctx* ctx) {
+  if (g_active == ctx || ctx->class_mu.empty()) return STK_OK;
+  double mu[256], imu[256];
+  for (int q = 0; q < 256; ++q) mu[q] = imu[q] = 1.0;
+  for (size_t q = 0; q < ctx->class_mu.size(); ++q) {
+    mu[q] = ctx->class_mu[q];
+    imu[q] = 1.0 / ctx->class_mu[q];
+  }
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyToSymbol(c_mu, mu, sizeof(mu)));
+  CK(cudaMemcpyToSymbol(c_inv_mu, imu, sizeof(imu)));
+  g_active = ctx;
+  return STK_OK;
+}
+
 stk_status check(const stk_ctx* ctx, int need_state) {
   if (!ctx) return STK_EINVAL;
   if (ctx->state < need_state) {
     const_cast<stk_ctx*>(ctx)->err = "call order violated (create -> set_viscosity -> assemble)";
     return STK_ESTATE;
   }
+  if (need_state >= 1) return activate(const_cast<stk_ctx*>(ctx));
   return STK_OK;
 }
 
@@ -466,8 +483,8 @@ stk_status stk_set_viscosity(stk_ctx* ctx, const uint8_t* elem_class, const doub
     imu[q] = 1.0 / class_mu[q];
   }
   ctx->class_mu.assign(class_mu, class_mu + nclass);
-  CK(cudaMemcpyToSymbolAsync(c_mu, mu, sizeof(mu), 0, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyToSymbolAsync(c_inv_mu, imu, sizeof(imu), 0, cudaMemcpyHostToDevice, ctx->stream));
+  g_active = nullptr;
+  ST(activate(ctx));
   Level& L = ctx->lev[0];
   const size_t ncls = (size_t)(L.cz1 - L.cz0) * L.n * L.n * 6;
   CK(cudaMemcpyAsync(L.cls, elem_class, ncls, cudaMemcpyHostToDevice, ctx->stream));
@@ -509,7 +526,7 @@ stk_status stk_assemble(stk_ctx* ctx) {
   // constant subdomain stencils for the tiled kernels
   for (int l = 0; l < ctx->nlev; ++l) {
     Level& L = ctx->lev[l];
-    if (L.n >= 64) ST(assemble_stencils(ctx->cfg.form, L.h, ctx->cfg.delta, l, ctx->stream) ? STK_OK : STK_ECUDA);
+    if (L.n >= 64) ST(assemble_stencils(ctx->stream) ? STK_OK : STK_ECUDA);
   }
   // coarsest level: dense K (+ gauge row), Gauss-Jordan inverse
   Level& L = ctx->lev[ctx->nlev - 1];
@@ -774,6 +791,7 @@ stk_status stk_destroy(stk_ctx* ctx) {
   cudaFree(ctx->sums);
   cudaFreeHost(ctx->hsums);
   ctx->comm.destroy();
+  if (g_active == ctx) g_active = nullptr;
   delete ctx;
   return STK_OK;
 }

@@ -111,41 +111,38 @@ def test_load_vector(cfgname, n):
     assert np.abs(y - b_o.reshape(4, -1)).max() <= 1e-13 * np.abs(b_o).max()
 
 
+def _star_minmax(c):
+    """min/max class over the 24 tets incident to each vertex (c: [k][j][i][t])."""
+    m = c.shape[0]
+    M1 = m + 1
+    smin = np.full((M1,) * 3, 255)
+    smax = np.full((M1,) * 3, -1)
+    for dz in (0, 1):
+        for dy in (0, 1):
+            for dx in (0, 1):
+                corner = np.array([dx, dy, dz])
+                ts = [t for t in range(6) if any((fem.kuhn_vertices(t)[q] == corner).all() for q in range(4))]
+                sub = c[..., ts]
+                sl = (slice(dz, dz + m), slice(dy, dy + m), slice(dx, dx + m))
+                smin[sl] = np.minimum(smin[sl], sub.min(axis=3))
+                smax[sl] = np.maximum(smax[sl], sub.max(axis=3))
+    b = np.zeros((M1,) * 3, bool)
+    b[0], b[-1], b[:, 0], b[:, -1], b[:, :, 0], b[:, :, -1] = [True] * 6
+    return smin, smax, b
+
+
 def test_classification_and_coarse_classes():
     import paper_1604_07994_b200 as stk
     n = 64
     ctx, cfg, cls, _ = make_ctx("cfg4", n, "mod")
-    # irregular = boundary vertex or a star with more than one viscosity
-    c4 = cls.reshape(n, n, n, 6)
-    N1 = n + 1
-    star_min = np.full((N1, N1, N1), 255)
-    star_max = np.full((N1, N1, N1), -1)
-    for dz in (0, 1):
-        for dy in (0, 1):
-            for dx in (0, 1):
-                sl = (slice(dz, dz + n), slice(dy, dy + n), slice(dx, dx + n))
-                star_min[sl] = np.minimum(star_min[sl], c4.min(axis=3))
-                star_max[sl] = np.maximum(star_max[sl], c4.max(axis=3))
-    bnd = np.zeros((N1,) * 3, bool)
-    bnd[0], bnd[-1], bnd[:, 0], bnd[:, -1], bnd[:, :, 0], bnd[:, :, -1] = [True] * 6
-    irr = bnd | (star_min != star_max)
-    assert ctx.layout(0).n_irregular == int(irr.sum())
-    # coarse level classes == oracle majority rule, level by level (through the irregular counts)
+    # irregular = boundary vertex or a 24-tet star with more than one viscosity
+    smin, smax, bnd = _star_minmax(cls.reshape(n, n, n, 6))
+    assert ctx.layout(0).n_irregular == int((bnd | (smin != smax)).sum())
+    # coarse level classes == oracle majority rule, level by level (via the irregular counts)
     h = mg.Hierarchy(n, cls, cfg.class_mu, cfg.faces)
     for l, lev in enumerate(h.levels):
         m = lev.n
-        c = lev.cls.reshape(m, m, m, 6)
-        M1 = m + 1
-        smin = np.full((M1,) * 3, 255)
-        smax = np.full((M1,) * 3, -1)
-        for dz in (0, 1):
-            for dy in (0, 1):
-                for dx in (0, 1):
-                    sl = (slice(dz, dz + m), slice(dy, dy + m), slice(dx, dx + m))
-                    smin[sl] = np.minimum(smin[sl], c.min(axis=3))
-                    smax[sl] = np.maximum(smax[sl], c.max(axis=3))
-        b = np.zeros((M1,) * 3, bool)
-        b[0], b[-1], b[:, 0], b[:, -1], b[:, :, 0], b[:, :, -1] = [True] * 6
+        smin, smax, b = _star_minmax(lev.cls.reshape(m, m, m, 6))
         assert ctx.layout(l).n_irregular == int((b | (smin != smax)).sum())
 
 
@@ -214,3 +211,46 @@ def test_solve_cfg1_rate():
     b_o, b_g = rhs_oracle_and_gpu(ctx, cfg, cls, fcls, pr)
     xg, rep = ctx.solve(b_g, rtol=1e-8)
     assert rep.rel_res <= 1e-8 and rep.cycles <= 30 and 0 < rep.rho < 0.6
+
+
+@pytest.mark.parametrize("cfgname,n,form", [("cfg2", 64, "mod"), ("cfg3", 64, "grad"),
+                                            ("cfg2", 64, "sym"), ("cfg5", 128, "mod"),
+                                            ("cfg4", 128, "mod")])
+def test_tiled_smoother_and_vcycle_vs_matrix_free_oracle(cfgname, n, form):
+    """Tiled TMA kernels (levels n >= 64) against the oracle multigrid with
+    element-loop products (oracle.mg_mf): one Uzawa step, one V-cycle."""
+    from oracle import mg_mf
+    nc = 4 if form == "sym" else 2
+    ctx, cfg, cls, fcls = make_ctx(cfgname, n, form, kernel_mode=1, ncolors_u=nc)
+    h = mg_mf.MFHierarchy(n, cls, cfg.class_mu, cfg.faces, form=form, ncolors_u=nc)
+    pr = h.levels[0].prob
+    rng = np.random.default_rng(4)
+    x = np.where(pr.free, rng.uniform(-1, 1, 4 * pr.V), 0.0)
+    b = np.where(pr.free, rng.uniform(-1, 1, 4 * pr.V), 0.0) * 1e-3
+    xs_o = h.uzawa(h.levels[0], x, b)
+    xg = ctx.import_(x.reshape(4, -1))
+    bg = ctx.import_(b.reshape(4, -1))
+    ctx.smooth(xg, bg, 1)
+    err, errs = per_field_rel(ctx.export(xg), xs_o)
+    assert err <= 1e-12, errs
+    r_o = b - pr.apply(xs_o)
+    r_g = ctx.export(ctx.residual(xg, bg))
+    err, errs = per_field_rel(r_g, r_o)
+    assert err <= 1e-11, errs
+    xv_o = h.vcycle(b, xs_o)
+    ctx.vcycle(bg, xg)
+    err, errs = per_field_rel(ctx.export(xg), xv_o)
+    assert err <= 1e-10, errs
+
+
+def test_tiled_equals_generic_device_path():
+    """The two device paths (tiled constant stencils / generic element rows) agree."""
+    n = 128
+    ctx, cfg, cls, fcls = make_ctx("cfg4", n, "mod", kernel_mode=1)
+    x = synth.apply_input(cfg)
+    xv = ctx.import_(x)
+    y1 = ctx.export(ctx.apply(xv))
+    ctx.set_kernel_mode(0)
+    y0 = ctx.export(ctx.apply(xv))
+    err, errs = per_field_rel(y1, y0)
+    assert err <= 1e-13, errs
