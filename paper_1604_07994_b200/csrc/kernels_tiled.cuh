@@ -19,6 +19,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "stk_common.cuh"
 
 namespace stk {
@@ -136,6 +138,9 @@ struct StreamArgs {
   unsigned blocks;      // APPLY block mask
   int color, ncolors;   // VEL
   double omega;         // P2
+  int no_tma;           // debug: stage planes with plain loads instead of TMA
+  const double* inA;    // (no_tma) base of the staged fields
+  const double* inB;    // (no_tma, VEL) pressure field
 };
 
 // shared-memory fetch for row_generic: planes staged in the ring
@@ -227,7 +232,9 @@ __global__ void __launch_bounds__(NT, 2)
   constexpr int NF = OP == OP_P2 ? 1 : 4;
   constexpr uint32_t SLOT_BYTES = NF * FST * sizeof(double);
   constexpr uint32_t TX_BYTES = NF * PLANE * sizeof(double);  // bytes landed per plane
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  unsigned char* smem_raw =
+      smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);  // 1 KB aligned TMA destinations
   double* ring = reinterpret_cast<double*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + RING * SLOT_BYTES);
   int* irr_cnt = reinterpret_cast<int*>(bars + RING);
@@ -253,7 +260,23 @@ __global__ void __launch_bounds__(NT, 2)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  auto stage_plain = [&](int m) {  // debug path: cooperative plain loads, synchronous
+    const int s = m % RING;
+    const int zl = kb1 + m - g.z0 + 1;
+    for (int e = threadIdx.x; e < NF * PLANE; e += NT) {
+      const int f = e / PLANE, r = e % PLANE;
+      const int li = r % HX, lj = r / HX;
+      const int gi = i0 - 1 + li, gj = j0 - 1 + lj;
+      double v = 0.0;
+      if (gi >= 0 && gj >= 0 && gi <= g.n && gj <= g.n) {
+        const double* src = (OP == OP_VEL && f == 3) ? a.inB : a.inA + (OP == OP_VEL ? f : f) * g.fs;
+        v = src[(int64_t)zl * g.py + (int64_t)gj * g.px + gi];
+      }
+      ring[(s * NF + f) * FST + r] = v;
+    }
+  };
   auto issue = [&](int m) {
+    if (a.no_tma) return;
     if (m >= M) return;
     const int s = m % RING;
     const int zc = kb1 + m - g.z0 + 1;  // local plane index of the layout
@@ -300,7 +323,12 @@ __global__ void __launch_bounds__(NT, 2)
       }
     }
     const int s = m % RING;
-    mbar_wait(&bars[s], (m / RING) & 1);
+    if (a.no_tma) {
+      stage_plain(m);
+      __syncthreads();
+    } else {
+      mbar_wait(&bars[s], (m / RING) & 1);
+    }
     const double* pl = ring + s * NF * FST;
     accumulate<FORM, OP, 1>(acc0, pl, base);   // plane P is output P-1's z+1 plane
     accumulate<FORM, OP, 0>(acc1, pl, base);
@@ -457,7 +485,7 @@ inline bool assemble_stencils(cudaStream_t st) {
 
 inline size_t stream_smem(int op) {
   const int NF = op == OP_P2 ? 1 : 4;
-  return RING * NF * FST * sizeof(double) + RING * sizeof(uint64_t) + sizeof(int) * (1 + (TX + 1) * (TY + 1) + 8);
+  return 1024 + RING * NF * FST * sizeof(double) + RING * sizeof(uint64_t) + sizeof(int) * (1 + (TX + 1) * (TY + 1) + 8);
 }
 
 template <int FORM, int OP>
@@ -478,6 +506,10 @@ bool launch_stream_t(const DGrid& g, const double* inA, const double* inB, int n
   int chunks = (target + tiles - 1) / tiles;
   chunks = std::max(1, std::min(chunks, g.nzl / 8));
   StreamArgs a = a0;
+  static const int no_tma = getenv("STK_NO_TMA") ? atoi(getenv("STK_NO_TMA")) : 0;
+  a.no_tma = no_tma;
+  a.inA = inA;
+  a.inB = inB;
   a.kchunk = (g.nzl + chunks - 1) / chunks;
   chunks = (g.nzl + a.kchunk - 1) / a.kchunk;
   k_stream<FORM, OP><<<dim3(tiles, chunks), NT, sm, st>>>(mA, mB, g, a);
