@@ -4,7 +4,8 @@ import numpy as np
 import synth
 from oracle import capi
 import paper_1604_07994_b200 as stk
-from tests.gpu_util import make_ctx, per_field_rel
+sys.path.insert(0, "tests")
+from gpu_util import make_ctx, per_field_rel
 n = 64
 ctx, cfg, cls, _ = make_ctx("cfg4", n, "mod", kernel_mode=1)
 x = synth.apply_input(cfg)
