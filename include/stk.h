@@ -23,8 +23,9 @@
  *    hierarchy, stencils, interface data, coarse inverse and communicator.
  *  - Device vectors hold 4 fields (u1,u2,u3,p) in the padded z-slab layout
  *    returned by stk_layout (element (f,i,j,k) at
- *    f*field_stride + (k - z0 + 1)*pitch_y + j*pitch_x + i, doubles; planes
- *    k = z0-1 and z0+nz_local are halo planes owned by the neighbours).
+ *    f*field_stride + (k - z0 + 1)*pitch_y + (j + 1)*pitch_x + (i + 1), doubles;
+ *    planes k = z0-1 and z0+nz_local are halo planes owned by the neighbours,
+ *    column i = -1 and row j = -1 are an unused ghost frame).
  *    Allocate stk_layout(...).vec_len doubles per vector.
  *  - Velocity entries at Dirichlet vertices (closure of Dirichlet faces) are
  *    ignored on input (treated as 0) and written as 0 on output.  Pressure
@@ -135,8 +136,9 @@ stk_status stk_import(stk_ctx* ctx, int32_t level, const double* canon, int32_t 
 stk_status stk_export(stk_ctx* ctx, int32_t level, const double* dev_vec, double* canon,
                       int32_t where);
 
-/* Right-hand side b = (f_h, 0).  kind 0: nodal f (canonical
- * 3 x (n+1)^2 x nz_local device array), b_u = consistent mass * f.
+/* Right-hand side b = (f_h, 0).  kind 0: nodal f given as a
+ * device level vector (padded layout, fields 0..2 = f; halo planes are
+ * exchanged by the call), b_u = consistent mass * f.
  * kind 1: element-constant f: f_dev = uint8 forcing class per element (same
  * layout as stk_set_viscosity), table = host 3 x nftab doubles. */
 stk_status stk_load_vector(stk_ctx* ctx, int32_t kind, const void* f_dev, const double* table,

@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(NT, 2)
       double v = 0.0;
       if (gi >= 0 && gj >= 0 && gi <= g.n && gj <= g.n) {
         const double* src = (OP == OP_VEL && f == 3) ? a.inB : a.inA + (OP == OP_VEL ? f : f) * g.fs;
-        v = src[(int64_t)zl * g.py + (int64_t)gj * g.px + gi];
+        v = src[(int64_t)zl * g.py + (int64_t)(gj + 1) * g.px + (gi + 1)];
       }
       ring[(s * NF + f) * FST + r] = v;
     }
@@ -284,10 +284,11 @@ __global__ void __launch_bounds__(NT, 2)
     mbar_expect_tx(&bars[s], TX_BYTES);
     double* dst = ring + s * NF * FST;
     if (OP == OP_VEL) {
-      for (int f = 0; f < 3; ++f) tma_load_4d(dst + f * FST, &mapA, &bars[s], i0 - 1, j0 - 1, zc, f);  // u
-      tma_load_4d(dst + 3 * FST, &mapB, &bars[s], i0 - 1, j0 - 1, zc, 0);                            // p
+      // box origin (i0-1, j0-1) in vertex coordinates = (i0, j0) in the ghost-framed layout
+      for (int f = 0; f < 3; ++f) tma_load_4d(dst + f * FST, &mapA, &bars[s], i0, j0, zc, f);  // u
+      tma_load_4d(dst + 3 * FST, &mapB, &bars[s], i0, j0, zc, 0);                            // p
     } else {
-      for (int f = 0; f < NF; ++f) tma_load_4d(dst + f * FST, &mapA, &bars[s], i0 - 1, j0 - 1, zc, f);
+      for (int f = 0; f < NF; ++f) tma_load_4d(dst + f * FST, &mapA, &bars[s], i0, j0, zc, f);
     }
   };
   if (threadIdx.x == 0)
@@ -330,6 +331,22 @@ __global__ void __launch_bounds__(NT, 2)
       mbar_wait(&bars[s], (m / RING) & 1);
     }
     const double* pl = ring + s * NF * FST;
+    // inputs at Dirichlet velocity DoFs are ignored: zero them in the staged plane
+    if (NF == 4) {
+      const unsigned dm = g.dirmask;
+      const bool mplane = ((dm & 16u) && P == 0) || ((dm & 32u) && P == g.n);
+      const bool mx0 = (dm & 1u) && i0 == 0, mx1 = (dm & 2u) && last_x;
+      const bool my0 = (dm & 4u) && j0 == 0, my1 = (dm & 8u) && last_y;
+      if (mplane || mx0 || mx1 || my0 || my1) {
+        double* w = ring + s * NF * FST;
+        for (int e = threadIdx.x; e < 3 * PLANE; e += NT) {
+          const int f = e / PLANE, r = e % PLANE, li = r % HX, lj = r / HX;
+          if (mplane || (mx0 && li == 1) || (mx1 && li == TX + 1) || (my0 && lj == 1) || (my1 && lj == TY + 1))
+            w[f * FST + r] = 0.0;
+        }
+        __syncthreads();
+      }
+    }
     accumulate<FORM, OP, 1>(acc0, pl, base);   // plane P is output P-1's z+1 plane
     accumulate<FORM, OP, 0>(acc1, pl, base);
     accumulate<FORM, OP, -1>(acc2, pl, base);
@@ -451,7 +468,8 @@ inline PFN_encodeTiled encoder() {
 inline bool make_map(CUtensorMap* map, const double* base, const DGrid& g, int box_fields) {
   PFN_encodeTiled enc = encoder();
   if (!enc) return false;
-  cuuint64_t dims[4] = {(cuuint64_t)(g.n + 1), (cuuint64_t)(g.n + 1), (cuuint64_t)(g.nzl + 2), (cuuint64_t)box_fields};
+  // ghost-framed extent: positions 0..n+1 hold vertices -1..n (boxes never leave it)
+  cuuint64_t dims[4] = {(cuuint64_t)(g.n + 2), (cuuint64_t)(g.n + 2), (cuuint64_t)(g.nzl + 2), (cuuint64_t)box_fields};
   cuuint64_t strides[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.py * 8, (cuuint64_t)g.fs * 8};
   cuuint32_t box[4] = {HX, HY, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};

@@ -426,8 +426,8 @@ stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
     L.nzl = per + (r == Pn - 1 ? 1 : 0);
     L.cz0 = std::max(0, L.z0 - 1);
     L.cz1 = std::min(L.n, L.z0 + L.nzl);
-    L.px = ((L.n + 1 + 15) / 16) * 16;
-    L.py = L.px * (L.n + 1);
+    L.px = ((L.n + 3 + 15) / 16) * 16;  // ghost column i = -1, vertices 0..n, spare
+    L.py = L.px * (L.n + 2);             // ghost row j = -1, rows 0..n
     L.fs = (((int64_t)(L.nzl + 2) * L.py + 31) / 32) * 32;
     L.vlen = 4 * L.fs;
     const size_t ncls = (size_t)(L.cz1 - L.cz0) * L.n * L.n * 6;

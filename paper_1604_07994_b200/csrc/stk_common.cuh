@@ -7,7 +7,9 @@
 // mesh is the same Kuhn grid at h/2, so every level is structured.
 //
 // Layout of a level vector (z-slab of this rank): 4 fields (u1,u2,u3,p),
-//   f*fs + (k - z0 + 1)*py + j*px + i,   planes z0-1 and z0+nzl are halos.
+//   f*fs + (k - z0 + 1)*py + (j + 1)*px + (i + 1)
+// planes z0-1 and z0+nzl are halos; column i = -1 and row j = -1 are a zero
+// ghost frame so that every TMA box starts at non-negative coordinates.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -42,7 +44,7 @@ struct DGrid {
 };
 
 __device__ __forceinline__ int64_t vidx(const DGrid& g, int i, int j, int k) {
-  return (int64_t)(k - g.z0 + 1) * g.py + (int64_t)j * g.px + i;
+  return (int64_t)(k - g.z0 + 1) * g.py + (int64_t)(j + 1) * g.px + (i + 1);
 }
 
 __device__ __forceinline__ bool is_dirichlet(const DGrid& g, int i, int j, int k) {
