@@ -79,6 +79,8 @@ typedef struct {
   int32_t nu_pre, nu_post, nu_inc; /* V_var smoothing: nu + nu_inc * level (DESIGN R13) */
   double omega;       /* Schur-complement under-relaxation, 0.3 */
   int32_t ncolors_u;  /* velocity GS colours (i+j+k) mod ncolors_u: 2 (red-black) or 4 */
+  int32_t krylov;     /* 0: stk_solve iterates V-cycles; m > 0: right-preconditioned
+                         GMRES(m) with one V-cycle as preconditioner */
   int32_t rank, nranks; /* z-slab owner and number of ranks (one GPU each) */
   void* stream;       /* cudaStream_t; NULL = legacy default stream */
 } stk_config;
@@ -159,7 +161,9 @@ stk_status stk_restrict(stk_ctx* ctx, int32_t fine_level, const double* r_f, dou
 stk_status stk_prolong_add(stk_ctx* ctx, int32_t coarse_level, const double* x_c, double* x_f);
 /* one V_var cycle on the finest level, in place on x */
 stk_status stk_vcycle(stk_ctx* ctx, const double* b, double* x);
-/* V-cycles until ||b-Kx||/||b|| <= rtol (synchronous); gauge applied at the end */
+/* V-cycles (or GMRES iterations, cfg.krylov > 0; max_cycles bounds the number of
+ * preconditioner applications) until ||b-Kx||/||b|| <= rtol (synchronous);
+ * gauge applied at the end */
 stk_status stk_solve(stk_ctx* ctx, const double* b, double* x, double rtol, int32_t max_cycles,
                      stk_report* report);
 /* subtract the mu^-1-weighted mean pressure (Q of P:136); no-op with traction faces */
@@ -172,6 +176,15 @@ stk_status stk_norms(stk_ctx* ctx, int32_t level, const double* x, double* out);
 stk_status stk_set_kernel_mode(stk_ctx* ctx, int32_t mode);
 /* Number of kernels this context launched so far (evidence counter). */
 int64_t stk_launch_count(const stk_ctx* ctx);
+
+/* Event-timed kernel profile.  While enabled, every op brackets its kernel
+ * launches with CUDA events on cfg.stream.  stk_profile_read sums the records of
+ * one op (0 apply, 1 residual, 2 velocity colour pass, 3 pressure pass 1,
+ * 4 pressure pass 2, 5 restriction, 6 prolongation, 7 coarse solve,
+ * 8 reductions, 9 Krylov vector ops) on one level (-1 = all); synchronises. */
+stk_status stk_profile_enable(stk_ctx* ctx, int32_t on);
+stk_status stk_profile_reset(stk_ctx* ctx);
+stk_status stk_profile_read(stk_ctx* ctx, int32_t op, int32_t level, int64_t* launches, double* ms);
 
 const char* stk_last_error(const stk_ctx* ctx);
 stk_status stk_destroy(stk_ctx* ctx);

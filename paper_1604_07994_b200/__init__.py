@@ -36,7 +36,7 @@ class stk_config(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("n_coarse", ctypes.c_int32), ("form", ctypes.c_int32),
                 ("face", ctypes.c_int32 * 6), ("delta", ctypes.c_double),
                 ("nu_pre", ctypes.c_int32), ("nu_post", ctypes.c_int32), ("nu_inc", ctypes.c_int32),
-                ("omega", ctypes.c_double), ("ncolors_u", ctypes.c_int32),
+                ("omega", ctypes.c_double), ("ncolors_u", ctypes.c_int32), ("krylov", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("stream", ctypes.c_void_p)]
 
 
@@ -76,6 +76,10 @@ _sigs = {
     "stk_gauge": [_P, ctypes.c_int32, _P],
     "stk_norms": [_P, ctypes.c_int32, _P, _P],
     "stk_set_kernel_mode": [_P, ctypes.c_int32],
+    "stk_profile_enable": [_P, ctypes.c_int32],
+    "stk_profile_reset": [_P],
+    "stk_profile_read": [_P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
+                         ctypes.POINTER(ctypes.c_double)],
     "stk_destroy": [_P],
 }
 for _name, _args in _sigs.items():
@@ -121,7 +125,7 @@ class StokesContext:
     """One rank (one GPU) of the distributed operator / solver."""
 
     def __init__(self, n, form="mod", faces=(0,) * 6, delta=1.0 / 12.0, n_coarse=4,
-                 nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2, rank=0, nranks=1,
+                 nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2, krylov=0, rank=0, nranks=1,
                  stream=None, nccl_id: bytes | None = None):
         import torch
         self.torch = torch
@@ -131,6 +135,7 @@ class StokesContext:
             cfg.face[f] = int(faces[f])
         cfg.delta, cfg.nu_pre, cfg.nu_post, cfg.nu_inc = delta, nu_pre, nu_post, nu_inc
         cfg.omega, cfg.ncolors_u, cfg.rank, cfg.nranks = omega, ncolors_u, rank, nranks
+        cfg.krylov = krylov
         if stream is None:
             stream = torch.cuda.current_stream()
         self.stream = stream
@@ -200,6 +205,22 @@ class StokesContext:
 
     def launch_count(self) -> int:
         return _lib.stk_launch_count(self.h)
+
+    PROFILE_OPS = ("apply", "residual", "vel_pass", "p_pass1", "p_pass2", "restrict", "prolong",
+                   "coarse", "reduce", "krylov")
+
+    def profile(self, on: bool = True):
+        self._chk("stk_profile_enable", _lib.stk_profile_enable(self.h, int(on)))
+
+    def profile_reset(self):
+        self._chk("stk_profile_reset", _lib.stk_profile_reset(self.h))
+
+    def profile_read(self, op, level=-1):
+        """(launches, total ms) of one op ('vel_pass', ...) on a level (-1 = all)."""
+        q = self.PROFILE_OPS.index(op) if isinstance(op, str) else op
+        n, ms = ctypes.c_int64(), ctypes.c_double()
+        self._chk("stk_profile_read", _lib.stk_profile_read(self.h, q, level, ctypes.byref(n), ctypes.byref(ms)))
+        return n.value, ms.value
 
     # -- vectors --------------------------------------------------------------
     def import_(self, canon, level=0, out=None):

@@ -139,6 +139,7 @@ struct StreamArgs {
   int color, ncolors;   // VEL
   double omega;         // P2
   int no_tma;           // debug: stage planes with plain loads instead of TMA
+  int skip_irr;         // debug (timing only): skip the irregular rows
   const double* inA;    // (no_tma) base of the staged fields
   const double* inB;    // (no_tma, VEL) pressure field
 };
@@ -397,7 +398,7 @@ __global__ void __launch_bounds__(NT, 2)
       if (last_x && last_y && threadIdx.x == 0) irr_list[atomicAdd(irr_cnt, 1)] = (TY + 1) * HX + (TX + 1);
     }
     __syncthreads();
-    if (fin) {
+    if (fin && !a.skip_irr) {
       const int cnt = *irr_cnt;
       for (int q = threadIdx.x; q < cnt; q += NT) {
         const int e = irr_list[q];
@@ -526,6 +527,8 @@ bool launch_stream_t(const DGrid& g, const double* inA, const double* inB, int n
   StreamArgs a = a0;
   static const int no_tma = getenv("STK_NO_TMA") ? atoi(getenv("STK_NO_TMA")) : 0;
   a.no_tma = no_tma;
+  static const int skip_irr = getenv("STK_SKIP_IRR") ? atoi(getenv("STK_SKIP_IRR")) : 0;
+  a.skip_irr = skip_irr;
   a.inA = inA;
   a.inB = inB;
   a.kchunk = (g.nzl + chunks - 1) / chunks;

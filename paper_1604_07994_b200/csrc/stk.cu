@@ -14,6 +14,7 @@
 #include "comm.cuh"
 #include "kernels_generic.cuh"
 #include "kernels_tiled.cuh"
+#include "krylov.cuh"
 
 using namespace stk;
 
@@ -32,6 +33,40 @@ struct Level {
   double* r = nullptr;    // scratch: residual / smoother temporaries
   int64_t nirr = 0;
   bool replicated = false;  // whole level held by every rank (coarse agglomeration)
+};
+
+// event-timed profile of the kernels launched while enabled (stk_profile_*)
+enum { P_APPLY = 0, P_RESID, P_VEL, P_P1, P_P2, P_RESTRICT, P_PROLONG, P_COARSE, P_REDUCE, P_KRYLOV, P_NOPS };
+struct ProfRec {
+  int op, level;
+  cudaEvent_t e0, e1;
+};
+struct Prof {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void reset() {
+    for (auto& r : recs) {
+      pool.push_back(r.e0);
+      pool.push_back(r.e1);
+    }
+    recs.clear();
+  }
+  void destroy() {
+    reset();
+    for (auto e : pool) cudaEventDestroy(e);
+    pool.clear();
+  }
 };
 
 }  // namespace
@@ -58,7 +93,35 @@ struct stk_ctx {
   double* hsums = nullptr;  // pinned
   int nparts = 0;
   Comm comm;
+  Prof prof;
+  // Krylov workspace (GMRES(m), cfg.krylov = m)
+  double* kbasis = nullptr;  // (m+1) level-0 vectors
+  double* kwork = nullptr;   // 3 level-0 vectors: w, z, r
+  double* kcoef = nullptr;   // device coefficients
+  double* kpart = nullptr;   // partial dot products
 };
+
+namespace {
+// RAII: brackets the kernel launches of one op with CUDA events when profiling
+struct PScope {
+  stk_ctx* c;
+  int op, lv;
+  cudaEvent_t e0 = nullptr;
+  PScope(stk_ctx* c_, int op_, int lv_) : c(c_), op(op_), lv(lv_) {
+    if (c->prof.on) {
+      e0 = c->prof.get();
+      cudaEventRecord(e0, c->stream);
+    }
+  }
+  ~PScope() {
+    if (c->prof.on && e0) {
+      cudaEvent_t e1 = c->prof.get();
+      cudaEventRecord(e1, c->stream);
+      c->prof.recs.push_back({op, lv, e0, e1});
+    }
+  }
+};
+}  // namespace
 
 namespace {
 
@@ -170,6 +233,7 @@ stk_status op_apply(stk_ctx* ctx, int l, unsigned blocks, const double* x, doubl
   Level& L = ctx->lev[l];
   ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, const_cast<double*>(x), 0, 4, L.replicated));
   DGrid g = dgrid(ctx, L);
+  PScope ps(ctx, P_APPLY, l);
   if (use_tiled(ctx, L)) {
     ST(launch_apply_tiled(ctx->cfg.form, g, x, y, blocks, ctx->stream) ? STK_OK : STK_EUNSUP);
     return launched(ctx);
@@ -187,6 +251,7 @@ stk_status op_residual(stk_ctx* ctx, int l, const double* x, const double* b, do
   Level& L = ctx->lev[l];
   ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, const_cast<double*>(x), 0, 4, L.replicated));
   DGrid g = dgrid(ctx, L);
+  PScope ps(ctx, P_RESID, l);
   if (use_tiled(ctx, L)) {
     ST(launch_residual_tiled(ctx->cfg.form, g, x, b, r, ctx->stream) ? STK_OK : STK_EUNSUP);
     return launched(ctx);
@@ -217,6 +282,7 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
     const double* uin = (pass & 1) ? tmp : x;
     double* uout = (pass & 1) ? x : tmp;
     ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, const_cast<double*>(uin), 0, 3, L.replicated));
+    PScope ps(ctx, P_VEL, l);
     if (tiled) {
       ST(launch_vel_pass_tiled(ctx->cfg.form, g, uin, p, b, uout, color, nc, ctx->stream) ? STK_OK
                                                                                            : STK_EUNSUP);
@@ -233,6 +299,8 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
   ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, x, 0, 3, L.replicated));
   double* T = tmp + 3 * L.fs;
   const double* gp = b + 3 * L.fs;
+  {
+  PScope ps(ctx, P_P1, l);
   if (tiled) {
     ST(launch_p_pass1_tiled(ctx->cfg.form, g, x, gp, T, ctx->stream) ? STK_OK : STK_EUNSUP);
   } else {
@@ -243,7 +311,9 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
     }
   }
   ST(launched(ctx));
+  }
   ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, tmp, 3, 1, L.replicated));
+  PScope ps2(ctx, P_P2, l);
   if (tiled) {
     ST(launch_p_pass2_tiled(ctx->cfg.form, g, T, p, ctx->cfg.omega, ctx->stream) ? STK_OK : STK_EUNSUP);
   } else {
@@ -262,6 +332,7 @@ stk_status op_restrict(stk_ctx* ctx, int lf, const double* rf, double* bc) {
     ST(ctx->comm.restrict_to_replicated(ctx, dgrid(ctx, F), dgrid(ctx, C), rf, bc));
     return STK_OK;
   }
+  PScope ps(ctx, P_RESTRICT, lf);
   k_restrict<<<nblocks(owned_vertices(C)), kThreads, 0, ctx->stream>>>(dgrid(ctx, F), dgrid(ctx, C), rf, bc);
   return launched(ctx);
 }
@@ -272,6 +343,7 @@ stk_status op_prolong_add(stk_ctx* ctx, int lc, const double* xc, double* xf) {
   ST(ctx->comm.halo(ctx, C.n, C.z0, C.nzl, C.py, C.fs, const_cast<double*>(xc), 0, 4, C.replicated));
   DGrid gc = dgrid(ctx, C);
   if (C.replicated && !F.replicated) gc = ctx->comm.replicated_view(gc);
+  PScope ps(ctx, P_PROLONG, lc);
   k_prolong_add<<<nblocks(owned_vertices(F)), kThreads, 0, ctx->stream>>>(gc, dgrid(ctx, F), xc, xf);
   return launched(ctx);
 }
@@ -279,6 +351,7 @@ stk_status op_prolong_add(stk_ctx* ctx, int lc, const double* xc, double* xf) {
 stk_status op_coarse(stk_ctx* ctx, const double* b, double* x) {
   Level& L = ctx->lev[ctx->nlev - 1];
   const size_t sh = sizeof(double) * ctx->cN;
+  PScope ps(ctx, P_COARSE, ctx->nlev - 1);
   k_coarse_apply<<<1, 1024, sh, ctx->stream>>>(dgrid(ctx, L), ctx->cdofs, ctx->cN, ctx->cN1, ctx->cG, b, x);
   return launched(ctx);
 }
@@ -287,6 +360,7 @@ stk_status op_coarse(stk_ctx* ctx, const double* b, double* x) {
 stk_status op_partials(stk_ctx* ctx, int l, const double* x, int with_gauge) {
   Level& L = ctx->lev[l];
   DGrid g = dgrid(ctx, L);
+  PScope ps(ctx, P_REDUCE, l);
   k_partials<<<ctx->nparts, 256, 0, ctx->stream>>>(g, x, ctx->part, with_gauge);
   ST(launched(ctx));
   k_partials_final<<<1, 256, 0, ctx->stream>>>(ctx->part, ctx->nparts, ctx->sums);
@@ -316,6 +390,144 @@ stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x) {
   ST(op_vcycle(ctx, l + 1, C.b, C.x));
   ST(op_prolong_add(ctx, l + 1, C.x, x));
   for (int s = 0; s < nu_post; ++s) ST(op_uzawa(ctx, l, x, b));
+  return STK_OK;
+}
+
+// ---- outer Krylov iteration ----------------------------------------------------
+
+constexpr int kDotBlocks = 296;
+
+// host out[q] = <V_q, w> over owned entries, all ranks (synchronises)
+stk_status op_dots(stk_ctx* ctx, const double* V, int nv, const double* w, double* out) {
+  Level& L = ctx->lev[0];
+  DGrid g = dgrid(ctx, L);
+  PScope ps(ctx, P_KRYLOV, 0);
+  for (int c0 = 0; c0 < nv; c0 += KRY_CHUNK) {
+    const int m = std::min(KRY_CHUNK, nv - c0);
+    k_dots<<<kDotBlocks, 256, 0, ctx->stream>>>(g, V + (int64_t)c0 * L.vlen, L.vlen, m, w, ctx->kpart);
+    ST(launched(ctx));
+    k_dots_final<<<1, 32, 0, ctx->stream>>>(ctx->kpart, kDotBlocks, m, ctx->kcoef + c0);
+    ST(launched(ctx));
+  }
+  if (!L.replicated) ST(ctx->comm.allreduce_sum(ctx, ctx->kcoef, nv));
+  CK(cudaMemcpyAsync(out, ctx->kcoef, sizeof(double) * nv, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return STK_OK;
+}
+
+// w = alpha w - sum_q c[q] V_q  (c on the host)
+stk_status op_update(stk_ctx* ctx, const double* V, int nv, const double* c, double alpha, double* w) {
+  Level& L = ctx->lev[0];
+  DGrid g = dgrid(ctx, L);
+  PScope ps(ctx, P_KRYLOV, 0);
+  CK(cudaMemcpyAsync(ctx->kcoef, c, sizeof(double) * nv, cudaMemcpyHostToDevice, ctx->stream));
+  for (int c0 = 0; c0 < nv || c0 == 0; c0 += KRY_CHUNK) {
+    const int m = std::min(KRY_CHUNK, nv - c0);
+    k_update<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(g, V + (int64_t)c0 * L.vlen, L.vlen, m,
+                                                                         ctx->kcoef + c0, c0 == 0 ? alpha : 1.0, w);
+    ST(launched(ctx));
+    if (nv == 0) break;
+  }
+  return STK_OK;
+}
+
+stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x);
+
+// Right-preconditioned restarted GMRES(m) on K x = b with M^-1 = one V_var cycle
+// from a zero guess (a fixed linear map).  CGS2 orthogonalisation, Givens rotations;
+// the correction x += M^-1 (V y) costs one extra cycle per restart.
+stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int max_its, stk_report* R,
+                    double bnorm, int& its, double& rel) {
+  Level& L = ctx->lev[0];
+  const int m = ctx->cfg.krylov;
+  const int64_t vlen = L.vlen;
+  const size_t vb = sizeof(double) * vlen;
+  if (!ctx->kbasis) {
+    if (cudaMalloc(&ctx->kbasis, vb * (m + 1)) != cudaSuccess || cudaMalloc(&ctx->kwork, vb * 3) != cudaSuccess ||
+        cudaMalloc(&ctx->kcoef, sizeof(double) * (m + 2 + KRY_CHUNK)) != cudaSuccess ||
+        cudaMalloc(&ctx->kpart, sizeof(double) * kDotBlocks * KRY_CHUNK) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->err = "out of device memory for the GMRES basis (reduce cfg.krylov)";
+      return STK_ENOMEM;
+    }
+    CK(cudaMemsetAsync(ctx->kbasis, 0, vb * (m + 1), ctx->stream));
+    CK(cudaMemsetAsync(ctx->kwork, 0, vb * 3, ctx->stream));
+  }
+  double* w = ctx->kwork;
+  double* z = ctx->kwork + vlen;
+  double* r = ctx->kwork + 2 * vlen;
+  auto V = [&](int q) { return ctx->kbasis + (int64_t)q * vlen; };
+  DGrid g0 = dgrid(ctx, L);
+  const unsigned nb = nblocks(owned_vertices(L));
+  std::vector<double> H((m + 1) * m, 0.0), cs(m), sn(m), gv(m + 1), h(m + 1), h2(m + 1), y(m);
+  double nr;
+  ST(op_residual(ctx, 0, x, b, r));
+  ST(op_dots(ctx, r, 1, r, &nr));
+  double beta = std::sqrt(nr);
+  rel = bnorm > 0 ? beta / bnorm : 0.0;
+  while (rel > rtol && its < max_its) {
+    k_axpby<<<nb, kThreads, 0, ctx->stream>>>(g0, 1.0 / beta, r, 0.0, V(0));
+    ST(launched(ctx));
+    std::fill(gv.begin(), gv.end(), 0.0);
+    gv[0] = beta;
+    int jdone = 0;
+    for (int j = 0; j < m && its < max_its; ++j) {
+      CK(cudaMemsetAsync(z, 0, vb, ctx->stream));
+      ST(op_vcycle(ctx, 0, V(j), z));
+      ST(op_apply(ctx, 0, BLK_ALL, z, w));
+      ST(op_dots(ctx, V(0), j + 1, w, h.data()));
+      ST(op_update(ctx, V(0), j + 1, h.data(), 1.0, w));
+      ST(op_dots(ctx, V(0), j + 1, w, h2.data()));
+      ST(op_update(ctx, V(0), j + 1, h2.data(), 1.0, w));
+      for (int q = 0; q <= j; ++q) h[q] += h2[q];
+      double ww;
+      ST(op_dots(ctx, w, 1, w, &ww));
+      h[j + 1] = std::sqrt(ww);
+      if (h[j + 1] > 0) {
+        k_axpby<<<nb, kThreads, 0, ctx->stream>>>(g0, 1.0 / h[j + 1], w, 0.0, V(j + 1));
+        ST(launched(ctx));
+      }
+      for (int q = 0; q < j; ++q) {  // previous rotations
+        const double t = cs[q] * h[q] + sn[q] * h[q + 1];
+        h[q + 1] = -sn[q] * h[q] + cs[q] * h[q + 1];
+        h[q] = t;
+      }
+      const double den = std::hypot(h[j], h[j + 1]);
+      cs[j] = den > 0 ? h[j] / den : 1.0;
+      sn[j] = den > 0 ? h[j + 1] / den : 0.0;
+      h[j] = den;
+      h[j + 1] = 0.0;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      for (int q = 0; q <= j; ++q) H[q * m + j] = h[q];
+      ++its;
+      jdone = j + 1;
+      rel = bnorm > 0 ? std::fabs(gv[j + 1]) / bnorm : 0.0;
+      if (its < 256) R->res_hist[its] = rel;
+      if (!std::isfinite(rel)) {
+        R->nan_seen = 1;
+        return STK_OK;
+      }
+      if (rel <= rtol) break;
+    }
+    // y = H^-1 g (upper triangular), x += M^-1 (V y)
+    for (int q = jdone - 1; q >= 0; --q) {
+      double s = gv[q];
+      for (int c = q + 1; c < jdone; ++c) s -= H[q * m + c] * y[c];
+      y[q] = s / H[q * m + q];
+    }
+    for (int q = 0; q < jdone; ++q) y[q] = -y[q];
+    ST(op_update(ctx, V(0), jdone, y.data(), 0.0, w));  // w = sum y_q V_q
+    CK(cudaMemsetAsync(z, 0, vb, ctx->stream));
+    ST(op_vcycle(ctx, 0, w, z));
+    k_axpby<<<nb, kThreads, 0, ctx->stream>>>(g0, 1.0, z, 1.0, x);
+    ST(launched(ctx));
+    ST(op_residual(ctx, 0, x, b, r));
+    ST(op_dots(ctx, r, 1, r, &nr));
+    beta = std::sqrt(nr);
+    rel = bnorm > 0 ? beta / bnorm : 0.0;  // true residual after the restart
+    if (its < 256) R->res_hist[its] = rel;
+  }
   return STK_OK;
 }
 
@@ -373,6 +585,7 @@ stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
   if (cfg->form < 0 || cfg->form > 2) return STK_EINVAL;
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return STK_EINVAL;
   if (cfg->ncolors_u != 2 && cfg->ncolors_u != 4) return STK_EINVAL;
+  if (cfg->krylov < 0 || cfg->krylov > 200) return STK_EINVAL;
   const int nc = cfg->n_coarse > 0 ? cfg->n_coarse : 4;
   if (nc > n || (nc & (nc - 1)) != 0 || nc > 16) return STK_EINVAL;
   bool any_dir = false;
@@ -734,15 +947,19 @@ stk_status stk_solve(stk_ctx* ctx, const double* b, double* x, double rtol, int3
   R->res_hist[0] = rel;
   int cyc = 0;
   stk_status st = STK_OK;
-  while (rel > rtol && cyc < max_cycles) {
-    ST(op_vcycle(ctx, 0, b, x));
-    ST(stk_residual(ctx, 0, x, b, L.r, nr));
-    ++cyc;
-    rel = bnorm > 0 ? std::sqrt(nr[4]) / bnorm : 0.0;
-    if (cyc < 256) R->res_hist[cyc] = rel;
-    if (!std::isfinite(rel)) {
-      R->nan_seen = 1;
-      break;
+  if (ctx->cfg.krylov > 0) {
+    ST(op_gmres(ctx, b, x, rtol, max_cycles, R, bnorm, cyc, rel));
+  } else {
+    while (rel > rtol && cyc < max_cycles) {
+      ST(op_vcycle(ctx, 0, b, x));
+      ST(stk_residual(ctx, 0, x, b, L.r, nr));
+      ++cyc;
+      rel = bnorm > 0 ? std::sqrt(nr[4]) / bnorm : 0.0;
+      if (cyc < 256) R->res_hist[cyc] = rel;
+      if (!std::isfinite(rel)) {
+        R->nan_seen = 1;
+        break;
+      }
     }
   }
   ST(op_gauge(ctx, 0, x));
@@ -772,6 +989,36 @@ stk_status stk_set_kernel_mode(stk_ctx* ctx, int32_t mode) {
 
 int64_t stk_launch_count(const stk_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+stk_status stk_profile_enable(stk_ctx* ctx, int32_t on) {
+  if (!ctx) return STK_EINVAL;
+  ctx->prof.on = on != 0;
+  return STK_OK;
+}
+
+stk_status stk_profile_reset(stk_ctx* ctx) {
+  if (!ctx) return STK_EINVAL;
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->prof.reset();
+  return STK_OK;
+}
+
+stk_status stk_profile_read(stk_ctx* ctx, int32_t op, int32_t level, int64_t* launches, double* ms) {
+  if (!ctx || !launches || !ms) return STK_EINVAL;
+  CK(cudaStreamSynchronize(ctx->stream));
+  int64_t cnt = 0;
+  double tot = 0.0;
+  for (auto& r : ctx->prof.recs) {
+    if (r.op != op || (level >= 0 && r.level != level)) continue;
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, r.e0, r.e1));
+    tot += t;
+    ++cnt;
+  }
+  *launches = cnt;
+  *ms = tot;
+  return STK_OK;
+}
+
 const char* stk_last_error(const stk_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 stk_status stk_destroy(stk_ctx* ctx) {
@@ -791,6 +1038,11 @@ stk_status stk_destroy(stk_ctx* ctx) {
   cudaFree(ctx->sums);
   cudaFreeHost(ctx->hsums);
   ctx->comm.destroy();
+  ctx->prof.destroy();
+  cudaFree(ctx->kbasis);
+  cudaFree(ctx->kwork);
+  cudaFree(ctx->kcoef);
+  cudaFree(ctx->kpart);
   if (g_active == ctx) g_active = nullptr;
   delete ctx;
   return STK_OK;

@@ -31,6 +31,24 @@ __constant__ int8_t c_corner_m[8][6];
 __constant__ int8_t c_child_off[6][8];
 __constant__ int8_t c_child_t[6][8];
 
+// compile-time Kuhn tables (the __constant__ copies above serve the setup kernels)
+__host__ __device__ constexpr int kperm(int t, int q) {
+  return t == 0 ? (q == 0 ? 0 : q == 1 ? 1 : 2)
+       : t == 1 ? (q == 0 ? 0 : q == 1 ? 2 : 1)
+       : t == 2 ? (q == 0 ? 1 : q == 1 ? 0 : 2)
+       : t == 3 ? (q == 0 ? 1 : q == 1 ? 2 : 0)
+       : t == 4 ? (q == 0 ? 2 : q == 1 ? 0 : 1)
+                : (q == 0 ? 2 : q == 1 ? 1 : 0);
+}
+// local index of cube corner c (bit0 x, bit1 y, bit2 z) in Kuhn tet t, or -1
+__host__ __device__ constexpr int kcorner(int c, int t) {
+  return c == 0 ? 0
+       : c == 7 ? 3
+       : c == (1 << kperm(t, 0)) ? 1
+       : c == ((1 << kperm(t, 0)) | (1 << kperm(t, 1))) ? 2
+                                                        : -1;
+}
+
 struct DGrid {
   int n;            // intervals of this level
   int z0, nzl;      // owned vertex planes [z0, z0+nzl)
@@ -89,20 +107,24 @@ __device__ __forceinline__ void row_generic(const DGrid& g, int i, int j, int k,
   y[0] = y[1] = y[2] = y[3] = 0.0;
   dA[0] = dA[1] = dA[2] = 0.0;
   dC = 0.0;
+#pragma unroll
   for (int dz = -1; dz <= 0; ++dz) {
     const int ck = k + dz;
     if (ck < 0 || ck >= g.n) continue;
+#pragma unroll
     for (int dy = -1; dy <= 0; ++dy) {
       const int cj = j + dy;
       if (cj < 0 || cj >= g.n) continue;
+#pragma unroll
       for (int dx = -1; dx <= 0; ++dx) {
         const int ci = i + dx;
         if (ci < 0 || ci >= g.n) continue;
         const int corner = (-dx) | ((-dy) << 1) | ((-dz) << 2);
+#pragma unroll
         for (int t = 0; t < 6; ++t) {
-          const int m = c_corner_m[corner][t];
+          const int m = kcorner(corner, t);
           if (m < 0) continue;
-          const int s1 = c_perm[t][0], s2 = c_perm[t][1], s3 = c_perm[t][2];
+          const int s1 = kperm(t, 0), s2 = kperm(t, 1), s3 = kperm(t, 2);
           int v[4][3];
           v[0][0] = ci; v[0][1] = cj; v[0][2] = ck;
           v[1][0] = ci; v[1][1] = cj; v[1][2] = ck; v[1][s1] += 1;

@@ -185,10 +185,10 @@ def element_classes(cfg: Config, k0: int = 0, k1: int | None = None):
     return mu.reshape(-1), fc.reshape(-1)
 
 
-def nodal_forcing(cfg: Config) -> np.ndarray:
-    """f_a(v) = 2 U(1, 3v+a) - 1, shape (3, V)."""
-    V = cfg.vertices
-    v = np.arange(V, dtype=np.uint64)
+def nodal_forcing(cfg: Config, v0: int = 0, v1: int | None = None) -> np.ndarray:
+    """f_a(v) = 2 U(1, 3v+a) - 1 for vertices v0..v1-1, shape (3, v1-v0)."""
+    v1 = cfg.vertices if v1 is None else v1
+    v = np.arange(v0, v1, dtype=np.uint64)
     return np.stack([2.0 * uniform(cfg.seed, 1, 3 * v + a) - 1.0 for a in range(3)])
 
 

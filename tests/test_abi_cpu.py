@@ -56,7 +56,7 @@ def test_create_rejects_bad_config_without_device():
         _fields_ = [("n", ctypes.c_int32), ("n_coarse", ctypes.c_int32), ("form", ctypes.c_int32),
                     ("face", ctypes.c_int32 * 6), ("delta", ctypes.c_double),
                     ("nu_pre", ctypes.c_int32), ("nu_post", ctypes.c_int32), ("nu_inc", ctypes.c_int32),
-                    ("omega", ctypes.c_double), ("ncolors_u", ctypes.c_int32),
+                    ("omega", ctypes.c_double), ("ncolors_u", ctypes.c_int32), ("krylov", ctypes.c_int32),
                     ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("stream", ctypes.c_void_p)]
 
     lib.stk_create.argtypes = [ctypes.POINTER(Cfg), ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]

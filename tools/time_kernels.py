@@ -12,6 +12,7 @@ import paper_1604_07994_b200 as stk
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 512
 mode = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+do_solve = not (len(sys.argv) > 4 and sys.argv[4] == "nosolve")
 cfg = synth.get_config(name, n=n)
 t0 = time.time()
 cls, fcls = synth.element_classes(cfg)
@@ -51,6 +52,8 @@ ms = timeit(lambda: ctx.residual(x, b, y))
 print(f"residual: {ms:.3f} ms  {97*V/ms/1e6:.0f} GB/s (97 B/vertex)", flush=True)
 ms = timeit(lambda: ctx.smooth(x, b, 1), reps=5)
 print(f"uzawa step: {ms:.3f} ms  ({ms/6:.3f} per pass avg)", flush=True)
+if not do_solve:
+    sys.exit(0)
 bb = ctx.load_nodal(synth.nodal_forcing(cfg)) if cfg.forcing == "nodal" else ctx.load_element(fcls, cfg.force_table)
 torch.cuda.synchronize()
 xs, rep = ctx.solve(bb, rtol=1e-8, max_cycles=60)
