@@ -1,11 +1,12 @@
-"""Minimal driver for ncu: a few applies + one Uzawa step on cfg4 (n=512)."""
+"""Minimal driver for ncu: a few applies + one Uzawa step.  usage: prof_apply.py [cfg] [n]"""
 import sys
 sys.path.insert(0, ".")
 import torch
 import synth
 import paper_1604_07994_b200 as stk
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
-cfg = synth.get_config("cfg4", n=n)
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 128
+cfg = synth.get_config(name, n=n)
 cls, _ = synth.element_classes(cfg)
 ctx = stk.StokesContext(n, "mod", cfg.faces)
 ctx.set_viscosity(cls, cfg.class_mu)
