@@ -340,32 +340,56 @@ __global__ void k_coarsen_classes(DGrid gf, DGrid gc, int ncz, uint8_t* __restri
   cls_c[tid] = cl[best];
 }
 
-// per-vertex code: regular class k (interior vertex whose 24 incident tets share
-// mu_k) or CODE_IRREGULAR (interface Gamma_12, boundary / Gamma_F rows);
-// counts irregular vertices into *nirr
+// per-vertex code (R6): class k (< 0x80) when
+// the star of tets inside the cube is isoviscous with class k AND the vertex is
+// interior or lies only on Dirichlet faces (then its velocity rows are
+// eliminated and its pressure row is the truncated constant stencil), else
+// CODE_IRREGULAR (Gamma_12, Gamma_F, classes >= 0x80): a list row evaluated by
+// the element loop.  Counts list rows into *nirr.
 __global__ void k_classify(DGrid g, uint8_t* __restrict__ code, unsigned long long* nirr) {
   int i, j, k;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (!owned_vertex(g, tid, i, j, k)) return;
   uint8_t c = CODE_IRREGULAR;
-  if (i > 0 && j > 0 && k > 0 && i < g.n && j < g.n && k < g.n) {
+  const unsigned m = g.dirmask;
+  const bool faces_ok = (i > 0 || (m & 1u)) && (i < g.n || (m & 2u)) && (j > 0 || (m & 4u)) &&
+                        (j < g.n || (m & 8u)) && (k > 0 || (m & 16u)) && (k < g.n || (m & 32u));
+  if (faces_ok) {
     bool same = true;
     int first = -1;
-    for (int dz = -1; dz <= 0; ++dz)
-      for (int dy = -1; dy <= 0; ++dy)
+    for (int dz = -1; dz <= 0; ++dz) {
+      const int ck = k + dz;
+      if (ck < 0 || ck >= g.n) continue;
+      for (int dy = -1; dy <= 0; ++dy) {
+        const int cj = j + dy;
+        if (cj < 0 || cj >= g.n) continue;
         for (int dx = -1; dx <= 0; ++dx) {
+          const int ci = i + dx;
+          if (ci < 0 || ci >= g.n) continue;
           const int corner = (-dx) | ((-dy) << 1) | ((-dz) << 2);
           for (int t = 0; t < 6; ++t) {
             if (c_corner_m[corner][t] < 0) continue;
-            const int cl = elem_class(g, i + dx, j + dy, k + dz, t);
+            const int cl = elem_class(g, ci, cj, ck, t);
             if (first < 0) first = cl;
             else if (cl != first && c_mu[cl] != c_mu[first]) same = false;
           }
         }
-    if (same) c = (uint8_t)first;
+      }
+    }
+    if (same && first >= 0 && first < 0x80) c = (uint8_t)first;
   }
   code[vidx(g, i, j, k)] = c;
   if (c == CODE_IRREGULAR) atomicAdd(nirr, 1ull);
+}
+
+// compact list of the owned list rows (CODE_IRREGULAR), as owned linear indices
+// t = (k - z0) (n+1)^2 + j (n+1) + i; *cnt must be zeroed.  Order is irrelevant:
+// every row is evaluated independently.
+__global__ void k_build_list(DGrid g, int32_t* __restrict__ list, unsigned long long* cnt) {
+  int i, j, k;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (!owned_vertex(g, tid, i, j, k)) return;
+  if (g.code[vidx(g, i, j, k)] == CODE_IRREGULAR) list[atomicAdd(cnt, 1ull)] = (int32_t)tid;
 }
 
 // ---- coarsest level: dense assembly, Gauss-Jordan inverse, apply -----------

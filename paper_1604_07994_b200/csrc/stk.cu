@@ -32,6 +32,7 @@ struct Level {
   double* b = nullptr;    // MG rhs (levels >= 1)
   double* r = nullptr;    // scratch: residual / smoother temporaries
   int64_t nirr = 0;
+  int32_t* list = nullptr;  // owned list rows (CODE_IRREGULAR), tiled levels only
   bool replicated = false;  // whole level held by every rank (coarse agglomeration)
 };
 
@@ -225,6 +226,8 @@ void host_tables(int8_t perm[6][3], int8_t corner[8][6], int8_t choff[6][8], int
 
 // ---- level operations ------------------------------------------------------
 
+ListView lview(const Level& L) { return ListView{L.list, (int)L.nirr}; }
+
 bool use_tiled(const stk_ctx* ctx, const Level& L) {
   return ctx->kernel_mode == 1 && L.n >= 64 && !L.replicated && tiled_supported(L.n);
 }
@@ -235,7 +238,7 @@ stk_status op_apply(stk_ctx* ctx, int l, unsigned blocks, const double* x, doubl
   DGrid g = dgrid(ctx, L);
   PScope ps(ctx, P_APPLY, l);
   if (use_tiled(ctx, L)) {
-    ST(launch_apply_tiled(ctx->cfg.form, g, x, y, blocks, ctx->stream) ? STK_OK : STK_EUNSUP);
+    ST(launch_apply_tiled(ctx->cfg.form, g, lview(L), x, y, blocks, ctx->stream) ? STK_OK : STK_EUNSUP);
     return launched(ctx);
   }
   const unsigned nb = nblocks(owned_vertices(L));
@@ -253,7 +256,7 @@ stk_status op_residual(stk_ctx* ctx, int l, const double* x, const double* b, do
   DGrid g = dgrid(ctx, L);
   PScope ps(ctx, P_RESID, l);
   if (use_tiled(ctx, L)) {
-    ST(launch_residual_tiled(ctx->cfg.form, g, x, b, r, ctx->stream) ? STK_OK : STK_EUNSUP);
+    ST(launch_residual_tiled(ctx->cfg.form, g, lview(L), x, b, r, ctx->stream) ? STK_OK : STK_EUNSUP);
     return launched(ctx);
   }
   const unsigned nb = nblocks(owned_vertices(L));
@@ -284,7 +287,7 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
     ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, const_cast<double*>(uin), 0, 3, L.replicated));
     PScope ps(ctx, P_VEL, l);
     if (tiled) {
-      ST(launch_vel_pass_tiled(ctx->cfg.form, g, uin, p, b, uout, color, nc, ctx->stream) ? STK_OK
+      ST(launch_vel_pass_tiled(ctx->cfg.form, g, lview(L), uin, p, b, uout, color, nc, ctx->stream) ? STK_OK
                                                                                            : STK_EUNSUP);
     } else {
       switch (ctx->cfg.form) {
@@ -302,7 +305,7 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
   {
   PScope ps(ctx, P_P1, l);
   if (tiled) {
-    ST(launch_p_pass1_tiled(ctx->cfg.form, g, x, gp, T, ctx->stream) ? STK_OK : STK_EUNSUP);
+    ST(launch_p_pass1_tiled(ctx->cfg.form, g, lview(L), x, gp, T, ctx->stream) ? STK_OK : STK_EUNSUP);
   } else {
     switch (ctx->cfg.form) {
       case FORM_MOD: k_p_pass1_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, x, gp, T); break;
@@ -315,7 +318,7 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
   ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, tmp, 3, 1, L.replicated));
   PScope ps2(ctx, P_P2, l);
   if (tiled) {
-    ST(launch_p_pass2_tiled(ctx->cfg.form, g, T, p, ctx->cfg.omega, ctx->stream) ? STK_OK : STK_EUNSUP);
+    ST(launch_p_pass2_tiled(ctx->cfg.form, g, lview(L), T, p, ctx->cfg.omega, ctx->stream) ? STK_OK : STK_EUNSUP);
   } else {
     k_p_pass2_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, T, p, ctx->cfg.omega);
   }
@@ -736,6 +739,21 @@ stk_status stk_assemble(stk_ctx* ctx) {
   CK(cudaStreamSynchronize(ctx->stream));
   cudaFree(dcnt);
   for (int l = 0; l < ctx->nlev; ++l) ctx->lev[l].nirr = (int64_t)cnt[l];
+  // compact list rows of the tiled levels (the list role of k_stream)
+  for (int l = 0; l < ctx->nlev; ++l) {
+    Level& L = ctx->lev[l];
+    cudaFree(L.list);
+    L.list = nullptr;
+    if (L.n < 64 || L.nirr == 0) continue;
+    CK(cudaMalloc(&L.list, sizeof(int32_t) * L.nirr));
+    unsigned long long* lc;
+    CK(cudaMalloc(&lc, sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(lc, 0, sizeof(unsigned long long), ctx->stream));
+    k_build_list<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), L.list, lc);
+    ST(launched(ctx));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(lc);
+  }
   // constant subdomain stencils for the tiled kernels
   for (int l = 0; l < ctx->nlev; ++l) {
     Level& L = ctx->lev[l];
@@ -1026,6 +1044,7 @@ stk_status stk_destroy(stk_ctx* ctx) {
   for (auto& L : ctx->lev) {
     cudaFree(L.cls);
     cudaFree(L.code);
+    cudaFree(L.list);
     cudaFree(L.x);
     cudaFree(L.b);
     cudaFree(L.r);

@@ -64,6 +64,9 @@ struct DGrid {
 __device__ __forceinline__ int64_t vidx(const DGrid& g, int i, int j, int k) {
   return (int64_t)(k - g.z0 + 1) * g.py + (int64_t)(j + 1) * g.px + (i + 1);
 }
+inline int64_t vidx_host(const DGrid& g, int i, int j, int k) {
+  return (int64_t)(k - g.z0 + 1) * g.py + (int64_t)(j + 1) * g.px + (i + 1);
+}
 
 __device__ __forceinline__ bool is_dirichlet(const DGrid& g, int i, int j, int k) {
   const unsigned m = g.dirmask;

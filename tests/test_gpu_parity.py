@@ -131,19 +131,31 @@ def _star_minmax(c):
     return smin, smax, b
 
 
-def test_classification_and_coarse_classes():
-    import paper_1604_07994_b200 as stk
+def _list_rows(c, faces):
+    """Expected list-row mask (R6): the star of tets inside the cube
+    holds more than one class, or the vertex lies on a traction face."""
+    smin, smax, _ = _star_minmax(c)
+    m1 = c.shape[0] + 1
+    trac = np.zeros((m1,) * 3, bool)          # [k][j][i]
+    sl = [(slice(None), slice(None), 0), (slice(None), slice(None), -1),
+          (slice(None), 0, slice(None)), (slice(None), -1, slice(None)),
+          (0, slice(None), slice(None)), (-1, slice(None), slice(None))]
+    for f in range(6):
+        if int(faces[f]) == 1:
+            trac[sl[f]] = True
+    return (smin != smax) | trac
+
+
+@pytest.mark.parametrize("cfgname", ["cfg4", "cfg2"])
+def test_classification_and_coarse_classes(cfgname):
     n = 64
-    ctx, cfg, cls, _ = make_ctx("cfg4", n, "mod")
-    # irregular = boundary vertex or a 24-tet star with more than one viscosity
-    smin, smax, bnd = _star_minmax(cls.reshape(n, n, n, 6))
-    assert ctx.layout(0).n_irregular == int((bnd | (smin != smax)).sum())
-    # coarse level classes == oracle majority rule, level by level (via the irregular counts)
+    ctx, cfg, cls, _ = make_ctx(cfgname, n, "mod")
+    assert ctx.layout(0).n_irregular == int(_list_rows(cls.reshape(n, n, n, 6), cfg.faces).sum())
+    # coarse level classes == oracle majority rule, level by level (via the list-row counts)
     h = mg.Hierarchy(n, cls, cfg.class_mu, cfg.faces)
     for l, lev in enumerate(h.levels):
         m = lev.n
-        smin, smax, b = _star_minmax(lev.cls.reshape(m, m, m, 6))
-        assert ctx.layout(l).n_irregular == int((b | (smin != smax)).sum())
+        assert ctx.layout(l).n_irregular == int(_list_rows(lev.cls.reshape(m, m, m, 6), cfg.faces).sum())
 
 
 @pytest.mark.parametrize("cfgname,form,mode", [("cfg1", "mod", 0), ("cfg2", "mod", 1),
