@@ -69,8 +69,8 @@ __global__ void k_coarsen_part(DGrid gf, DGrid gc, int CK0, int CK1, uint8_t* __
   int best = 0;
   for (int q = 1; q < 8; ++q) {
     const bool better = cnt[q] > cnt[best] ||
-                        (cnt[q] == cnt[best] && (c_mu[cl[q]] > c_mu[cl[best]] ||
-                                                 (c_mu[cl[q]] == c_mu[cl[best]] && cl[q] < cl[best])));
+                        (cnt[q] == cnt[best] && (mu_of(gf, cl[q]) > mu_of(gf, cl[best]) ||
+                                                 (mu_of(gf, cl[q]) == mu_of(gf, cl[best]) && cl[q] < cl[best])));
     if (better) best = q;
   }
   cls_c[((((int64_t)(CK - gc.cz0)) * nc + CJ) * nc + CI) * 6 + T] = cl[best];

@@ -333,19 +333,21 @@ __global__ void k_coarsen_classes(DGrid gf, DGrid gc, int ncz, uint8_t* __restri
   int best = 0;
   for (int q = 1; q < 8; ++q) {
     const bool better = cnt[q] > cnt[best] ||
-                        (cnt[q] == cnt[best] && (c_mu[cl[q]] > c_mu[cl[best]] ||
-                                                 (c_mu[cl[q]] == c_mu[cl[best]] && cl[q] < cl[best])));
+                        (cnt[q] == cnt[best] && (mu_of(gf, cl[q]) > mu_of(gf, cl[best]) ||
+                                                 (mu_of(gf, cl[q]) == mu_of(gf, cl[best]) && cl[q] < cl[best])));
     if (better) best = q;
   }
   cls_c[tid] = cl[best];
 }
 
-// per-vertex code (R6): class k (< 0x80) when
+// per-vertex code (R6): class k (< 0x40) when
 // the star of tets inside the cube is isoviscous with class k AND the vertex is
 // interior or lies only on Dirichlet faces (then its velocity rows are
-// eliminated and its pressure row is the truncated constant stencil), else
-// CODE_IRREGULAR (Gamma_12, Gamma_F, classes >= 0x80): a list row evaluated by
-// the element loop.  Counts list rows into *nirr.
+// eliminated and its pressure row is the truncated constant stencil);
+// 0x40 | k for an isoviscous vertex of the traction top face z = 1 that lies on
+// no other face (truncated constant stencils of the 4 cubes below); else
+// CODE_IRREGULAR (Gamma_12, other Gamma_F rows, classes >= 0x40): a list row
+// evaluated by the element loop.  Counts list rows into *nirr.
 __global__ void k_classify(DGrid g, uint8_t* __restrict__ code, unsigned long long* nirr) {
   int i, j, k;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -354,7 +356,9 @@ __global__ void k_classify(DGrid g, uint8_t* __restrict__ code, unsigned long lo
   const unsigned m = g.dirmask;
   const bool faces_ok = (i > 0 || (m & 1u)) && (i < g.n || (m & 2u)) && (j > 0 || (m & 4u)) &&
                         (j < g.n || (m & 8u)) && (k > 0 || (m & 16u)) && (k < g.n || (m & 32u));
-  if (faces_ok) {
+  // a vertex on the traction top face z = 1 and on no other face (Gamma_F)
+  const bool top = k == g.n && !(m & 32u) && i > 0 && i < g.n && j > 0 && j < g.n;
+  if (faces_ok || top) {
     bool same = true;
     int first = -1;
     for (int dz = -1; dz <= 0; ++dz) {
@@ -371,12 +375,18 @@ __global__ void k_classify(DGrid g, uint8_t* __restrict__ code, unsigned long lo
             if (c_corner_m[corner][t] < 0) continue;
             const int cl = elem_class(g, ci, cj, ck, t);
             if (first < 0) first = cl;
-            else if (cl != first && c_mu[cl] != c_mu[first]) same = false;
+            else if (cl != first && mu_of(g, cl) != mu_of(g, first)) same = false;
           }
         }
       }
     }
-    if (same && first >= 0 && first < 0x80) c = (uint8_t)first;
+    if (same && first >= 0) {
+      if (top) {
+        if (first < 0x40) c = (uint8_t)(0x40 | first);   // CODE_TOP | class
+      } else if (first < 0x40) {
+        c = (uint8_t)first;
+      }
+    }
   }
   code[vidx(g, i, j, k)] = c;
   if (c == CODE_IRREGULAR) atomicAdd(nirr, 1ull);

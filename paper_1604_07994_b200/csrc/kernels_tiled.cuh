@@ -1,13 +1,12 @@
 // Tiled constant-stencil kernels for levels with n >= 64 (the hot path).
 //
 // Design:
-//  * One launch = two CTA roles.  The first `list_blocks` CTAs evaluate the
-//    rows of the compact list of irregular vertices (interface Gamma_12, the
-//    traction boundary Gamma_F, vertices touching both kinds of faces) by the
-//    element loop row_generic, one row per thread, reading the input vector
-//    from global memory (L2).  The remaining CTAs stream the grid.  The two
-//    write disjoint rows, so they need no synchronisation and the hardware
-//    back-fills stream CTAs as soon as the list CTAs retire.
+//  * List rows (interface Gamma_12, the traction boundary Gamma_F, vertices
+//    touching both kinds of faces) are evaluated by a second kernel, k_list:
+//    one row per thread by the cube-major element loop row_list (exact element
+//    formulas), reading the input from global memory (L2).  The two kernels
+//    write disjoint rows; k_list runs after k_stream on the same stream (or
+//    concurrently on a forked side stream, STK_LIST_FORK=1).
 //  * A stream CTA owns a TX x TY column tile (i in [i0, i0+TX), j in
 //    [j0, j0+TY), i0+TX <= n) and a chunk of z-planes.  Each plane of the input
 //    fields, with a 1-vertex xy halo, is staged in shared memory by TMA boxes
@@ -33,7 +32,9 @@
 #pragma once
 #include <cuda.h>
 
+#include <cmath>
 #include <cstdlib>
+#include <vector>
 
 #include "stk_common.cuh"
 
@@ -45,8 +46,81 @@ constexpr int HX = TX + 2, HY = TY + 2, PLANE = HX * HY;
 constexpr int FST = ((PLANE + 15) / 16) * 16;
 constexpr int PREF = 3, RING = PREF + 2;
 
-// unit stencils (h = 1, mu = 1, delta = 1) of an interior vertex, offset index
-// o = (dz+1)*9 + (dy+1)*3 + (dx+1):  row (centre, a) / centre pressure row
+// Integer unit stencils of an interior vertex (h = 1, mu = 1, delta = 1), by
+// the element sum over the 24 tets of its star, evaluated at compile time:
+//   kind 0: 6 A_form[a][b](o), kind 1: 24 B^T[a](o), kind 2: 24 B[b](o), kind 3: 6 C(o)
+// (the factors 6 and 24 make every entry an integer: |T| = 1/6, B = -|T|/4 grad).
+// A regular row of class k scales them by mu_k h / 6, h^2 / 24, h^2 / 24 and
+// delta h^3 / (6 mu_k) ("interior stencils can be pre-computed").
+// k_assemble_stencils sums the same element matrices at run time in floating
+// point and stk_assemble checks the two agree (k_check_stencils).
+__host__ __device__ constexpr int kst(int kind, int form, int a, int b, int dx, int dy, int dz, int cmask = 0xFF) {
+  int s = 0;
+  for (int cz = -1; cz <= 0; ++cz)
+    for (int cy = -1; cy <= 0; ++cy)
+      for (int cx = -1; cx <= 0; ++cx) {
+        const int corner = (-cx) | ((-cy) << 1) | ((-cz) << 2);
+        if (!((cmask >> corner) & 1)) continue;  // cube absent (outside the domain)
+        for (int t = 0; t < 6; ++t) {
+          const int m = kcorner(corner, t);
+          if (m < 0) continue;
+          int gr[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+          const int s1 = kperm(t, 0), s2 = kperm(t, 1), s3 = kperm(t, 2);
+          gr[0][s1] = -1; gr[1][s1] = 1; gr[1][s2] = -1; gr[2][s2] = 1; gr[2][s3] = -1; gr[3][s3] = 1;
+          for (int q = 0; q < 4; ++q) {
+            const int c = ktet_corner(t, q);
+            if ((c & 1) + cx != dx || ((c >> 1) & 1) + cy != dy || (c >> 2) + cz != dz) continue;
+            const int gg = gr[m][0] * gr[q][0] + gr[m][1] * gr[q][1] + gr[m][2] * gr[q][2];
+            if (kind == 0) {
+              const int G = (a == b) ? gg : 0, S = gr[q][a] * gr[m][b], D = gr[m][a] * gr[q][b];
+              s += form == FORM_MOD ? G + S - D : form == FORM_SYM ? G + S : G;
+            } else if (kind == 1) {
+              s -= gr[m][a];
+            } else if (kind == 2) {
+              s -= gr[q][b];
+            } else {
+              s += gg;
+            }
+          }
+        }
+      }
+  return s;
+}
+template <int KIND, int FORM, int A, int B, int DX, int DY, int DZ>
+struct KS {
+  static constexpr double v = (double)kst(KIND, FORM, A, B, DX, DY, DZ);
+};
+// truncated stencils of a vertex on the top face z = 1 (only the 4 cubes below
+// it, own corners 4..7, lie in the domain): the rows of an isoviscous traction
+// top-face vertex (Gamma_F), evaluated by the same element sum
+constexpr int KTOP_MASK = 0xF0;
+template <int KIND, int FORM, int A, int B, int DX, int DY, int DZ>
+struct KT {
+  static constexpr double v = (double)kst(KIND, FORM, A, B, DX, DY, DZ, KTOP_MASK);
+};
+constexpr uint8_t CODE_TOP = 0x40;  // code bit: isoviscous traction top-face row (class in bits 0..5)
+// closed forms of SURVEY App. A.2 (compile-time checks of the element sums)
+constexpr bool kst_closed_forms_hold() {
+  for (int o = 0; o < 27; ++o) {
+    const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
+    const int nax = (dx != 0) + (dy != 0) + (dz != 0);
+    const int lap = nax == 0 ? 36 : nax == 1 ? -6 : 0;  // 6 x (6, -1, 0)
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        if (kst(0, FORM_GRAD, a, b, dx, dy, dz) != (a == b ? lap : 0)) return false;
+        if (kst(0, FORM_MOD, a, b, dx, dy, dz) != (a == b ? lap : 0)) return false;  // cross part 0
+      }
+    if (kst(3, 0, 0, 0, dx, dy, dz) != lap) return false;
+  }
+  // (Bu)(i) = h^2/24 sum_b sum_{d in D+} beta^b_d (u_b(i-d) - u_b(i+d)), beta = 6 (d = e_b),
+  // 2 (d_b = 1), -2 (d_b = 0); B^T p pairs p(i+d) - p(i-d) with the same beta
+  return kst(2, 0, 0, 0, 1, 0, 0) == -6 && kst(2, 0, 0, 1, 1, 0, 0) == 2 && kst(2, 0, 0, 0, 1, 1, 0) == -2 &&
+         kst(2, 0, 0, 0, -1, -1, -1) == 2 && kst(1, 0, 0, 0, 1, 0, 0) == 6 && kst(2, 0, 0, 0, 0, 0, 0) == 0;
+}
+static_assert(kst_closed_forms_hold(), "Kuhn unit stencils disagree with the closed forms");
+
+// run-time stencils assembled by k_assemble_stencils (floating point), checked
+// against kst by k_check_stencils
 __constant__ double st_A[3][3][3][27];  // [form][a][b][o]
 __constant__ double st_BT[3][27];       // velocity row a, pressure column
 __constant__ double st_B[3][27];        // pressure row, velocity column b
@@ -152,13 +226,11 @@ struct StreamArgs {
   const double* inP;    // input pressure (APPLY/RESID/VEL/P1) or T (P2)   [list role]
   const int32_t* list;  // irregular rows: owned linear vertex index
   int nlist;
-  int list_blocks;      // leading CTAs running the list role
   int kchunk;           // output planes per stream CTA
   unsigned blocks;      // APPLY block mask
   int color, ncolors;   // VEL
   double omega;         // P2
   int ux0, uy0, uz0;    // velocity tensor-map origin (vertex coordinates)
-  int skip_list;        // debug (timing only): skip the list role
 };
 
 // in-plane offsets of one streamed plane: (0,0) (1,0) (-1,0) (0,1) (0,-1) (1,1) (-1,-1)
@@ -173,7 +245,7 @@ __device__ __forceinline__ constexpr bool axis_or_centre(int dx, int dy, int dz)
 }
 __device__ __forceinline__ constexpr int oidx(int dx, int dy, int dz) { return (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1); }
 
-// accumulators of one output row (unscaled)
+// accumulators of one output row, in integer-stencil units (6A, 24B^T, 24B, 6C)
 struct Acc {
   double A[3], BT[3], B, C;
   __device__ __forceinline__ void zero() {
@@ -181,46 +253,66 @@ struct Acc {
   }
 };
 
-template <int FORM, int OP, int DZ>
-__device__ __forceinline__ void accumulate(Acc& acc, const double* __restrict__ pl, int base) {
-  constexpr bool NEED_U = OP != OP_P1 && OP != OP_P2;   // A, B^T rows
-  constexpr bool NEED_P = OP != OP_VEL;                 // B, C rows
-#pragma unroll
-  for (int q = 0; q < 7; ++q) {
-    const int dx = kdx(q), dy = kdy(q);
-    if (!kuhn(dx, dy, DZ)) continue;
-    const int o = oidx(dx, dy, DZ);
+// contribution of staged in-plane point Q (offset (kdx(Q), kdy(Q)) from the
+// output column, plane offset DZ from the output row) to one output row
+template <int FORM, int OP, int DZ, int Q>
+__device__ __forceinline__ void acc_q(Acc& acc, const double* __restrict__ pl, int base) {
+  constexpr int dx = kdx(Q), dy = kdy(Q);
+  if constexpr (kuhn(dx, dy, DZ)) {
+    constexpr bool NEED_U = OP != OP_P1 && OP != OP_P2;  // A, B^T rows
+    constexpr bool NEED_P = OP != OP_VEL;                // B, C rows
+    constexpr double kC = KS<3, 0, 0, 0, dx, dy, DZ>::v;
     const int s = base + dy * HX + dx;
-    if (OP == OP_P2) {
-      if (axis_or_centre(dx, dy, DZ)) acc.C += st_C[o] * pl[s];
-      continue;
-    }
-    const double u0 = pl[0 * FST + s], u1 = pl[1 * FST + s], u2 = pl[2 * FST + s];
-    const double p = pl[3 * FST + s];
-    if (NEED_U) {
-      if (FORM == FORM_SYM) {
-        const double uu[3] = {u0, u1, u2};
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b) acc.A[a] += st_A[FORM_SYM][a][b][o] * uu[b];
-      } else if (axis_or_centre(dx, dy, DZ)) {
-        const double L = st_A[FORM][0][0][o];
-        acc.A[0] += L * u0;
-        acc.A[1] += L * u1;
-        acc.A[2] += L * u2;
+    if constexpr (OP == OP_P2) {
+      if constexpr (kC != 0.0) acc.C = fma(kC, pl[s], acc.C);
+    } else {
+      const double u0 = pl[s], u1 = pl[FST + s], u2 = pl[2 * FST + s], p = pl[3 * FST + s];
+      if constexpr (NEED_U) {
+        if constexpr (FORM == FORM_SYM) {
+          acc.A[0] = fma(KS<0, FORM_SYM, 0, 0, dx, dy, DZ>::v, u0, acc.A[0]);
+          acc.A[0] = fma(KS<0, FORM_SYM, 0, 1, dx, dy, DZ>::v, u1, acc.A[0]);
+          acc.A[0] = fma(KS<0, FORM_SYM, 0, 2, dx, dy, DZ>::v, u2, acc.A[0]);
+          acc.A[1] = fma(KS<0, FORM_SYM, 1, 0, dx, dy, DZ>::v, u0, acc.A[1]);
+          acc.A[1] = fma(KS<0, FORM_SYM, 1, 1, dx, dy, DZ>::v, u1, acc.A[1]);
+          acc.A[1] = fma(KS<0, FORM_SYM, 1, 2, dx, dy, DZ>::v, u2, acc.A[1]);
+          acc.A[2] = fma(KS<0, FORM_SYM, 2, 0, dx, dy, DZ>::v, u0, acc.A[2]);
+          acc.A[2] = fma(KS<0, FORM_SYM, 2, 1, dx, dy, DZ>::v, u1, acc.A[2]);
+          acc.A[2] = fma(KS<0, FORM_SYM, 2, 2, dx, dy, DZ>::v, u2, acc.A[2]);
+        } else {
+          constexpr double kA = KS<0, FORM_GRAD, 0, 0, dx, dy, DZ>::v;  // = mod on regular rows
+          if constexpr (kA != 0.0) {
+            acc.A[0] = fma(kA, u0, acc.A[0]);
+            acc.A[1] = fma(kA, u1, acc.A[1]);
+            acc.A[2] = fma(kA, u2, acc.A[2]);
+          }
+        }
+        constexpr double kT0 = KS<1, 0, 0, 0, dx, dy, DZ>::v, kT1 = KS<1, 0, 1, 0, dx, dy, DZ>::v,
+                         kT2 = KS<1, 0, 2, 0, dx, dy, DZ>::v;
+        if constexpr (kT0 != 0.0) acc.BT[0] = fma(kT0, p, acc.BT[0]);
+        if constexpr (kT1 != 0.0) acc.BT[1] = fma(kT1, p, acc.BT[1]);
+        if constexpr (kT2 != 0.0) acc.BT[2] = fma(kT2, p, acc.BT[2]);
       }
-      if (!(dx == 0 && dy == 0 && DZ == 0)) {
-        acc.BT[0] += st_BT[0][o] * p;
-        acc.BT[1] += st_BT[1][o] * p;
-        acc.BT[2] += st_BT[2][o] * p;
+      if constexpr (NEED_P) {
+        constexpr double kB0 = KS<2, 0, 0, 0, dx, dy, DZ>::v, kB1 = KS<2, 0, 0, 1, dx, dy, DZ>::v,
+                         kB2 = KS<2, 0, 0, 2, dx, dy, DZ>::v;
+        if constexpr (kB0 != 0.0) acc.B = fma(kB0, u0, acc.B);
+        if constexpr (kB1 != 0.0) acc.B = fma(kB1, u1, acc.B);
+        if constexpr (kB2 != 0.0) acc.B = fma(kB2, u2, acc.B);
+        if constexpr (kC != 0.0) acc.C = fma(kC, p, acc.C);
       }
-    }
-    if (NEED_P) {
-      if (!(dx == 0 && dy == 0 && DZ == 0)) acc.B += st_B[0][o] * u0 + st_B[1][o] * u1 + st_B[2][o] * u2;
-      if (axis_or_centre(dx, dy, DZ)) acc.C += st_C[o] * p;
     }
   }
+}
+
+template <int FORM, int OP, int DZ>
+__device__ __forceinline__ void accumulate(Acc& acc, const double* __restrict__ pl, int base) {
+  acc_q<FORM, OP, DZ, 0>(acc, pl, base);
+  acc_q<FORM, OP, DZ, 1>(acc, pl, base);
+  acc_q<FORM, OP, DZ, 2>(acc, pl, base);
+  acc_q<FORM, OP, DZ, 3>(acc, pl, base);
+  acc_q<FORM, OP, DZ, 4>(acc, pl, base);
+  acc_q<FORM, OP, DZ, 5>(acc, pl, base);
+  acc_q<FORM, OP, DZ, 6>(acc, pl, base);
 }
 
 // Truncated-star C row of an isoviscous boundary vertex in unit form:
@@ -245,29 +337,41 @@ __device__ __forceinline__ void c_trunc(const double* pm, const double* p0, cons
   diag = (double)((X0 + X1) * wx + (Y0 + Y1) * wy + (Z0 + Z1) * wz);
 }
 
-// unit B row (sum_o sum_b st_B[b][o] u_b(v+o)) from three staged planes, for the
+// 24 x unit B row (sum_o sum_b kst(2,b,o) u_b(v+o)) from three staged planes, for the
 // face vertices i = n / j = n (SKIPX / SKIPY: offsets with dx = +1 / dy = +1 lie
 // outside the staged box; the zero-extended velocity vanishes there)
+template <int DX, int DY, int DZ, bool SKIPX, bool SKIPY>
+__device__ __forceinline__ void b_off(double& acc, const double* const pl[3], int s) {
+  if constexpr (kuhn(DX, DY, DZ) && !(DX == 0 && DY == 0 && DZ == 0) && !(SKIPX && DX == 1) && !(SKIPY && DY == 1)) {
+    const double* q = pl[DZ + 1] + s + DY * HX + DX;
+    acc = fma(KS<2, 0, 0, 0, DX, DY, DZ>::v, q[0 * FST], acc);
+    acc = fma(KS<2, 0, 0, 1, DX, DY, DZ>::v, q[1 * FST], acc);
+    acc = fma(KS<2, 0, 0, 2, DX, DY, DZ>::v, q[2 * FST], acc);
+  }
+}
+template <int DZ, bool SKIPX, bool SKIPY>
+__device__ __forceinline__ void b_plane(double& acc, const double* const pl[3], int s) {
+  b_off<-1, -1, DZ, SKIPX, SKIPY>(acc, pl, s);
+  b_off<0, -1, DZ, SKIPX, SKIPY>(acc, pl, s);
+  b_off<1, -1, DZ, SKIPX, SKIPY>(acc, pl, s);
+  b_off<-1, 0, DZ, SKIPX, SKIPY>(acc, pl, s);
+  b_off<0, 0, DZ, SKIPX, SKIPY>(acc, pl, s);
+  b_off<1, 0, DZ, SKIPX, SKIPY>(acc, pl, s);
+  b_off<-1, 1, DZ, SKIPX, SKIPY>(acc, pl, s);
+  b_off<0, 1, DZ, SKIPX, SKIPY>(acc, pl, s);
+  b_off<1, 1, DZ, SKIPX, SKIPY>(acc, pl, s);
+}
 template <bool SKIPX, bool SKIPY>
 __device__ __forceinline__ double b_row_smem(const double* const pl[3], int s) {
   double acc = 0.0;
-#pragma unroll
-  for (int dz = -1; dz <= 1; ++dz)
-#pragma unroll
-    for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-      for (int dx = -1; dx <= 1; ++dx) {
-        if (!kuhn(dx, dy, dz) || (dx == 0 && dy == 0 && dz == 0)) continue;
-        if ((SKIPX && dx == 1) || (SKIPY && dy == 1)) continue;
-        const int o = oidx(dx, dy, dz);
-        const double* q = pl[dz + 1] + s + dy * HX + dx;
-        acc += st_B[0][o] * q[0 * FST] + st_B[1][o] * q[1 * FST] + st_B[2][o] * q[2 * FST];
-      }
+  b_plane<-1, SKIPX, SKIPY>(acc, pl, s);
+  b_plane<0, SKIPX, SKIPY>(acc, pl, s);
+  b_plane<1, SKIPX, SKIPY>(acc, pl, s);
   return acc;
 }
 
 // finishes a Dirichlet boundary row with an isoviscous star of class `code`
-// (velocity rows are 0): Bu = unit B row (OP_APPLY/RESID/P1), planes pl[0..2]
+// (velocity rows are 0): Bu = 24 x unit B row (OP_APPLY/RESID/P1), planes pl[0..2]
 // = k-1, k, k+1 (4-field slots, or 1-field T slots for P2), s = smem position
 template <int OP>
 __device__ __forceinline__ void finish_boundary(const DGrid& g, const StreamArgs& a, int i, int j, int k,
@@ -277,11 +381,11 @@ __device__ __forceinline__ void finish_boundary(const DGrid& g, const StreamArgs
   constexpr int PF = OP == OP_P2 ? 0 : 3;  // pressure (or T) field within a slot
   double sum, diag;
   c_trunc(pl[0] + PF * FST, pl[1] + PF * FST, pl[2] + PF * FST, s, i, j, k, g.n, sum, diag);
-  const double cw = g.delta * h * h * h * c_inv_mu[code] * (1.0 / 6.0);  // per-count edge weight
+  const double cw = g.delta * h * h * h * imu_of(g, code) * (1.0 / 6.0);  // per-count edge weight
   const double pv = pl[1][PF * FST + s];
   if (OP == OP_APPLY || OP == OP_RESID) {
     const unsigned blk = OP == OP_APPLY ? a.blocks : BLK_ALL;
-    const double yp = ((blk & BLK_B) ? h * h * Bu : 0.0) - ((blk & BLK_C) ? cw * (diag * pv - sum) : 0.0);
+    const double yp = ((blk & BLK_B) ? (h * h / 24.0) * Bu : 0.0) - ((blk & BLK_C) ? cw * (diag * pv - sum) : 0.0);
     a.out[0 * g.fs + o] = 0.0;
     a.out[1 * g.fs + o] = 0.0;
     a.out[2 * g.fs + o] = 0.0;
@@ -291,7 +395,7 @@ __device__ __forceinline__ void finish_boundary(const DGrid& g, const StreamArgs
     a.out[1 * g.fs + o] = 0.0;
     a.out[2 * g.fs + o] = 0.0;
   } else if (OP == OP_P1) {
-    const double r = h * h * Bu - cw * (diag * pv - sum) - __ldg(a.aux + o);
+    const double r = (h * h / 24.0) * Bu - cw * (diag * pv - sum) - __ldg(a.aux + o);
     a.out[o] = ((i + j + k) & 1) == 0 ? r / (cw * diag) : r;
   } else {  // P2: pv = T_v; neighbours of a colour-1 vertex are colour 0
     double d = pv;
@@ -300,15 +404,14 @@ __device__ __forceinline__ void finish_boundary(const DGrid& g, const StreamArgs
   }
 }
 
-// ---- list role: irregular rows by the element loop -----------------------------
+// ---- list rows: irregular rows by the element loop, one row per thread -----------
 template <int FORM, int OP>
 __device__ __forceinline__ void list_row(const DGrid& g, const StreamArgs& a, int i, int j, int k) {
   const int64_t o = vidx(g, i, j, k);
   const bool dir = is_dirichlet(g, i, j, k);
   double y[4], dA[3], dC;
   if (OP == OP_APPLY || OP == OP_RESID) {
-    FetchVec fx{a.inU, a.inP};
-    row_generic<FORM>(g, i, j, k, fx, OP == OP_APPLY ? a.blocks : BLK_ALL, y, dA, dC);
+    row_list<FORM, false>(g, i, j, k, a.inU, a.inP, OP == OP_APPLY ? a.blocks : BLK_ALL, y, dA, dC);
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
       double v = y[f];
@@ -317,36 +420,32 @@ __device__ __forceinline__ void list_row(const DGrid& g, const StreamArgs& a, in
     }
   } else if (OP == OP_VEL) {
     const bool act = ((i + j + k) % a.ncolors) == a.color && !dir;
-    if (act) {
-      FetchVec fx{a.inU, a.inP};
-      row_generic<FORM>(g, i, j, k, fx, BLK_A | BLK_BT, y, dA, dC);
-    }
+    if (act) row_list<FORM, false>(g, i, j, k, a.inU, a.inP, BLK_A | BLK_BT, y, dA, dC);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double uc = dir ? 0.0 : __ldg(a.inU + c * g.fs + o);
       a.out[c * g.fs + o] = act ? uc + (__ldg(a.aux + c * g.fs + o) - y[c]) / dA[c] : uc;
     }
   } else if (OP == OP_P1) {
-    FetchVec fx{a.inU, a.inP};
-    row_generic<FORM>(g, i, j, k, fx, BLK_B | BLK_C, y, dA, dC);
+    row_list<FORM, false>(g, i, j, k, a.inU, a.inP, BLK_B | BLK_C, y, dA, dC);
     const double r = y[3] - __ldg(a.aux + o);
     a.out[o] = ((i + j + k) & 1) == 0 ? r / dC : r;
   } else {
     const double T = __ldg(a.inP + o);
     double d = T;
     if ((i + j + k) & 1) {
-      FetchRedP fx{a.inP};
-      row_generic<FORM>(g, i, j, k, fx, BLK_C, y, dA, dC);
+      row_list<FORM, true>(g, i, j, k, a.inU, a.inP, BLK_C, y, dA, dC);
       d = (T + y[3]) / dC;
     }
     a.out[o] += a.omega * d;
   }
 }
 
+constexpr int LIST_NT = 128;
 template <int FORM, int OP>
-__device__ __noinline__ void list_role(const DGrid& g, const StreamArgs& a) {
-  const int e = blockIdx.x * NT + threadIdx.x;
-  if (e >= a.nlist || a.skip_list) return;
+__global__ void __launch_bounds__(LIST_NT) k_list(DGrid g, StreamArgs a) {
+  const int e = blockIdx.x * LIST_NT + threadIdx.x;
+  if (e >= a.nlist) return;
   const int t = a.list[e];
   const int nx = g.n + 1;
   const int k = g.z0 + t / (nx * nx);
@@ -354,27 +453,170 @@ __device__ __noinline__ void list_role(const DGrid& g, const StreamArgs& a) {
   list_row<FORM, OP>(g, a, r % nx, r / nx, k);
 }
 
-// ---- stream role ----------------------------------------------------------------
+// ---- traction top-face rows (z = 1, isoviscous star): truncated stencils ----------
+template <int FORM, int OP, int DX, int DY, int DZ>
+__device__ __forceinline__ void top_off(Acc& acc, const double* const pls[3], int base) {
+  if constexpr (kuhn(DX, DY, DZ) && DZ <= 0) {
+    constexpr int NF = OP == OP_P2 ? 1 : 4;
+    const double* q = pls[DZ + 1] + base + DY * HX + DX;
+    if constexpr (OP == OP_P2) {
+      constexpr double kC = KT<3, 0, 0, 0, DX, DY, DZ>::v;
+      if constexpr (kC != 0.0) acc.C = fma(kC, q[0], acc.C);
+    } else {
+      const double u[3] = {q[0], q[FST], q[2 * FST]};
+      const double p = q[3 * FST];
+      (void)NF;
+      if constexpr (OP != OP_P1) {
+#define STK_TOP_A(a_, b_)                                                     \
+  {                                                                           \
+    constexpr double kA = KT<0, FORM, a_, b_, DX, DY, DZ>::v;                 \
+    if constexpr (kA != 0.0) acc.A[a_] = fma(kA, u[b_], acc.A[a_]);           \
+  }
+        STK_TOP_A(0, 0) STK_TOP_A(0, 1) STK_TOP_A(0, 2)
+        STK_TOP_A(1, 0) STK_TOP_A(1, 1) STK_TOP_A(1, 2)
+        STK_TOP_A(2, 0) STK_TOP_A(2, 1) STK_TOP_A(2, 2)
+#undef STK_TOP_A
+        constexpr double kT0 = KT<1, 0, 0, 0, DX, DY, DZ>::v, kT1 = KT<1, 0, 1, 0, DX, DY, DZ>::v,
+                         kT2 = KT<1, 0, 2, 0, DX, DY, DZ>::v;
+        if constexpr (kT0 != 0.0) acc.BT[0] = fma(kT0, p, acc.BT[0]);
+        if constexpr (kT1 != 0.0) acc.BT[1] = fma(kT1, p, acc.BT[1]);
+        if constexpr (kT2 != 0.0) acc.BT[2] = fma(kT2, p, acc.BT[2]);
+      }
+      if constexpr (OP != OP_VEL) {
+        constexpr double kB0 = KT<2, 0, 0, 0, DX, DY, DZ>::v, kB1 = KT<2, 0, 0, 1, DX, DY, DZ>::v,
+                         kB2 = KT<2, 0, 0, 2, DX, DY, DZ>::v, kC = KT<3, 0, 0, 0, DX, DY, DZ>::v;
+        if constexpr (kB0 != 0.0) acc.B = fma(kB0, u[0], acc.B);
+        if constexpr (kB1 != 0.0) acc.B = fma(kB1, u[1], acc.B);
+        if constexpr (kB2 != 0.0) acc.B = fma(kB2, u[2], acc.B);
+        if constexpr (kC != 0.0) acc.C = fma(kC, p, acc.C);
+      }
+    }
+  }
+}
+template <int FORM, int OP, int DZ>
+__device__ __forceinline__ void top_plane(Acc& acc, const double* const pls[3], int base) {
+  top_off<FORM, OP, -1, -1, DZ>(acc, pls, base);
+  top_off<FORM, OP, 0, -1, DZ>(acc, pls, base);
+  top_off<FORM, OP, 1, -1, DZ>(acc, pls, base);
+  top_off<FORM, OP, -1, 0, DZ>(acc, pls, base);
+  top_off<FORM, OP, 0, 0, DZ>(acc, pls, base);
+  top_off<FORM, OP, 1, 0, DZ>(acc, pls, base);
+  top_off<FORM, OP, -1, 1, DZ>(acc, pls, base);
+  top_off<FORM, OP, 0, 1, DZ>(acc, pls, base);
+  top_off<FORM, OP, 1, 1, DZ>(acc, pls, base);
+}
+// row of an isoviscous traction top-face vertex (code = CODE_TOP | class),
+// from the staged planes k-1 (pls[0]) and k (pls[1])
 template <int FORM, int OP>
-__global__ void __launch_bounds__(NT, 2)
-    k_stream(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapP, DGrid g,
-             StreamArgs a) {
-  if ((int)blockIdx.x < a.list_blocks) {
-    list_role<FORM, OP>(g, a);
+__device__ __forceinline__ void finish_top(const DGrid& g, const StreamArgs& a, int i, int j, int k, int64_t o,
+                                        uint8_t code, const double aux[4], const double* const pls[3], int base) {
+  Acc acc;
+  acc.zero();
+  top_plane<FORM, OP, -1>(acc, pls, base);
+  top_plane<FORM, OP, 0>(acc, pls, base);
+  const int cl = code & (CODE_TOP - 1);
+  const double h = g.h, mu = mu_of(g, cl), imu = imu_of(g, cl);
+  const double sA = mu * h * (1.0 / 6.0), sB = h * h * (1.0 / 24.0), sC = g.delta * h * h * h * imu * (1.0 / 6.0);
+  constexpr double kAd0 = KT<0, FORM, 0, 0, 0, 0, 0>::v, kAd1 = KT<0, FORM, 1, 1, 0, 0, 0>::v,
+                   kAd2 = KT<0, FORM, 2, 2, 0, 0, 0>::v, kCd = KT<3, 0, 0, 0, 0, 0, 0>::v;
+  if (OP == OP_APPLY || OP == OP_RESID) {
+    const unsigned blk = OP == OP_APPLY ? a.blocks : BLK_ALL;
+    double y[4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) y[c] = ((blk & BLK_A) ? sA * acc.A[c] : 0.0) + ((blk & BLK_BT) ? sB * acc.BT[c] : 0.0);
+    y[3] = ((blk & BLK_B) ? sB * acc.B : 0.0) - ((blk & BLK_C) ? sC * acc.C : 0.0);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) a.out[f * g.fs + o] = OP == OP_RESID ? aux[f] - y[f] : y[f];
+  } else if (OP == OP_VEL) {
+    const bool act = ((i + j + k) % a.ncolors) == a.color;
+    const double kd[3] = {kAd0, kAd1, kAd2};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double uc = pls[1][c * FST + base];
+      a.out[c * g.fs + o] = act ? uc + (aux[c] - fma(sA, acc.A[c], sB * acc.BT[c])) / (sA * kd[c]) : uc;
+    }
+  } else if (OP == OP_P1) {
+    const double r = fma(sB, acc.B, -sC * acc.C) - aux[3];
+    a.out[o] = ((i + j + k) & 1) == 0 ? r / (sC * kCd) : r;
+  } else {
+    const double T = pls[1][base];
+    double d = T;
+    if ((i + j + k) & 1) d = (T - sC * (acc.C - kCd * T)) / (sC * kCd);
+    a.out[o] = aux[3] + a.omega * d;
+  }
+}
+
+// ---- stream role ----------------------------------------------------------------
+
+// finishes output row k of this thread's column from the completed accumulator
+template <int FORM, int OP>
+__device__ __forceinline__ void finish_row(const DGrid& g, const StreamArgs& a, int i, int j, int k, int64_t o,
+                                           uint8_t code, const double aux[4], const Acc& acc,
+                                           const double* const pls[3], int base) {
+  const double h = g.h;
+  if (!(i > 0 && j > 0 && k > 0 && k < g.n)) {
+    finish_boundary<OP>(g, a, i, j, k, code, acc.B, pls, base);
     return;
   }
+  const double mu = mu_of(g, code), imu = imu_of(g, code);
+  const double sA = mu * h * (1.0 / 6.0);                       // 6A units
+  const double sB = h * h * (1.0 / 24.0);                       // 24B, 24B^T units
+  const double sC = g.delta * h * h * h * imu * (1.0 / 6.0);    // 6C units
+  constexpr double kAd0 = KS<0, FORM, 0, 0, 0, 0, 0>::v, kAd1 = KS<0, FORM, 1, 1, 0, 0, 0>::v,
+                   kAd2 = KS<0, FORM, 2, 2, 0, 0, 0>::v, kCd = KS<3, 0, 0, 0, 0, 0, 0>::v;
+  if (OP == OP_APPLY || OP == OP_RESID) {
+    double y[4];
+    if (OP == OP_RESID || a.blocks == BLK_ALL) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) y[c] = fma(sA, acc.A[c], sB * acc.BT[c]);
+      y[3] = fma(sB, acc.B, -sC * acc.C);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        y[c] = ((a.blocks & BLK_A) ? sA * acc.A[c] : 0.0) + ((a.blocks & BLK_BT) ? sB * acc.BT[c] : 0.0);
+      y[3] = ((a.blocks & BLK_B) ? sB * acc.B : 0.0) - ((a.blocks & BLK_C) ? sC * acc.C : 0.0);
+    }
+#pragma unroll
+    for (int f = 0; f < 4; ++f) a.out[f * g.fs + o] = OP == OP_RESID ? aux[f] - y[f] : y[f];
+  } else if (OP == OP_VEL) {
+    const bool act = ((i + j + k) % a.ncolors) == a.color;
+    const double* cpl = pls[1];
+    const double kd[3] = {kAd0, kAd1, kAd2};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double uc = cpl[c * FST + base];
+      double v = uc;
+      if (act) v = uc + (aux[c] - fma(sA, acc.A[c], sB * acc.BT[c])) / (sA * kd[c]);
+      a.out[c * g.fs + o] = v;
+    }
+  } else if (OP == OP_P1) {
+    const double r = fma(sB, acc.B, -sC * acc.C) - aux[3];
+    a.out[o] = ((i + j + k) & 1) == 0 ? r / (sC * kCd) : r;
+  } else {  // P2: acc.C = sum_o 6C(o) T (incl. the centre); neighbours of colour 1 are colour 0
+    const double T = pls[1][base];
+    double d = T;
+    if ((i + j + k) & 1) d = (T - sC * (acc.C - kCd * T)) / (sC * kCd);
+    a.out[o] = aux[3] + a.omega * d;
+  }
+}
+
+template <int FORM, int OP>
+__global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP == OP_VEL) ? 2 : 3)
+    k_stream(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapP, DGrid g,
+             StreamArgs a) {
   constexpr int NF = OP == OP_P2 ? 1 : 4;
+  constexpr int SLOT = NF * FST;
   constexpr uint32_t TX_BYTES = NF * PLANE * sizeof(double);  // bytes landed per plane
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* smem_raw =
       smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);  // 1 KB aligned TMA destinations
   double* ring = reinterpret_cast<double*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + RING * NF * FST * sizeof(double));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + RING * SLOT * sizeof(double));
 
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int ntx = g.n / TX;
   const int tiles = ntx * (g.n / TY);
-  const int sb = blockIdx.x - a.list_blocks;
+  const int sb = blockIdx.x;
   const int tile = sb % tiles, chunk = sb / tiles;   // chunk-major: neighbours share L2
   const int i0 = (tile % ntx) * TX, j0 = (tile / ntx) * TY;
   const int kb = g.z0 + chunk * a.kchunk;
@@ -385,11 +627,10 @@ __global__ void __launch_bounds__(NT, 2)
   const bool last_x = i0 + TX == g.n, last_y = j0 + TY == g.n;
   const int i = i0 + tx, j = j0 + ty;
   const int base = (ty + 1) * HX + (tx + 1);
-  const double h = g.h;
-  const double sA = h, sB = h * h, sC = g.delta * h * h * h;  // times mu / 1 / 1/mu
   // extra face rows: (n, j) for the last lane of last-x tiles, (i, n) for the
   // last warp of last-y tiles, (n, n) for the last thread of the corner tile
   const bool ex_x = last_x && tx == TX - 1, ex_y = last_y && ty == TY - 1, ex_c = ex_x && ex_y;
+  const bool any_ex = last_x || last_y;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RING; ++s) mbar_init(&bars[s], 1);
@@ -402,7 +643,7 @@ __global__ void __launch_bounds__(NT, 2)
     const int P = kb1 + m;
     fence_proxy_async();
     mbar_expect_tx(&bars[s], TX_BYTES);
-    double* dst = ring + s * NF * FST;
+    double* dst = ring + s * SLOT;
     if (NF == 4) {
       for (int f = 0; f < 3; ++f)
         tma_load_4d(dst + f * FST, &mapU, &bars[s], i0 - 1 - a.ux0, j0 - 1 - a.uy0, P - a.uz0, f);
@@ -412,111 +653,87 @@ __global__ void __launch_bounds__(NT, 2)
     }
   };
   if (threadIdx.x == 0)
-    for (int m = 0; m < PREF; ++m) issue(m);
+    for (int m = 0; m < RING; ++m) issue(m);  // every slot is free at the start
 
-  Acc acc0, acc1, acc2;  // outputs P-1, P, P+1
-  acc0.zero();
-  acc1.zero();
-  acc2.zero();
+  // iteration m (plane P = kb-1+m) uses accumulators (acc0, acc1, acc2) for
+  // outputs (P-1, P, P+1); R[] rotates by one per iteration (unrolled by 3)
+  Acc R0, R1, R2;
+  // m = 0 (plane kb-1): only output kb (its z-1 plane)
+  R2.zero();
+  mbar_wait(&bars[0], 0);
+  accumulate<FORM, OP, -1>(R2, ring, base);
+  // m = 1 (plane kb): outputs kb (in-plane) and kb+1 (z-1 plane)
+  R0.zero();
+  mbar_wait(&bars[1], 0);
+  accumulate<FORM, OP, 0>(R2, ring + SLOT, base);
+  accumulate<FORM, OP, -1>(R0, ring + SLOT, base);
+  int64_t o = vidx(g, i, j, kb);  // output row of the current iteration
 
-  for (int m = 0; m < M; ++m) {
-    const int P = kb1 + m;
-    const int k = P - 1;  // output finished in this iteration
-    const bool fin = m >= 2;
-    // early loads of per-output data (codes, own auxiliary values)
-    uint8_t code = CODE_IRREGULAR, code_x = CODE_IRREGULAR, code_y = CODE_IRREGULAR, code_c = CODE_IRREGULAR;
+  auto body = [&](int m, Acc& acc0, Acc& acc1, Acc& acc2) {
+    const int k = kb1 + m - 1;  // output finished in this iteration
+    acc2.zero();
+    // early loads of per-output data (codes, own auxiliary values); consumed
+    // only after the accumulation, so their latency hides behind it
+    const uint8_t code = __ldg(g.code + o);
+    uint8_t cxy[3] = {0xFF, 0xFF, 0xFF};
+    if (any_ex) {
+      if (ex_x) cxy[0] = __ldg(g.code + o + 1);
+      if (ex_y) cxy[1] = __ldg(g.code + o + g.px);
+      if (ex_c) cxy[2] = __ldg(g.code + o + g.px + 1);
+    }
     double aux[4] = {0, 0, 0, 0};
-    if (fin) {
-      const int64_t o = vidx(g, i, j, k);
-      code = __ldg(g.code + o);
-      if (ex_x) code_x = __ldg(g.code + o + 1);
-      if (ex_y) code_y = __ldg(g.code + o + g.px);
-      if (ex_c) code_c = __ldg(g.code + o + g.px + 1);
-      if (!(code & 0x80)) {
-        if (OP == OP_RESID) {
+    if (OP == OP_RESID) {
 #pragma unroll
-          for (int f = 0; f < 4; ++f) aux[f] = __ldg(a.aux + f * g.fs + o);
-        } else if (OP == OP_VEL) {
+      for (int f = 0; f < 4; ++f) aux[f] = __ldg(a.aux + f * g.fs + o);
+    } else if (OP == OP_VEL) {
 #pragma unroll
-          for (int f = 0; f < 3; ++f) aux[f] = __ldg(a.aux + f * g.fs + o);
-        } else if (OP == OP_P1) {
-          aux[3] = __ldg(a.aux + o);
-        } else if (OP == OP_P2) {
-          aux[3] = a.out[o];
-        }
-      }
+      for (int f = 0; f < 3; ++f) aux[f] = __ldg(a.aux + f * g.fs + o);
+    } else if (OP == OP_P1) {
+      aux[3] = __ldg(a.aux + o);
+    } else if (OP == OP_P2) {
+      aux[3] = a.out[o];
     }
     const int s = m % RING;
     mbar_wait(&bars[s], (m / RING) & 1);
-    const double* pl = ring + s * NF * FST;
-    accumulate<FORM, OP, 1>(acc0, pl, base);   // plane P is output P-1's z+1 plane
-    accumulate<FORM, OP, 0>(acc1, pl, base);
-    accumulate<FORM, OP, -1>(acc2, pl, base);
-
-    if (fin) {
-      const int64_t o = vidx(g, i, j, k);
-      const double* pls[3] = {ring + ((m - 2) % RING) * NF * FST, ring + ((m - 1) % RING) * NF * FST, pl};
-      if (!(code & 0x80)) {
-        const bool interior = i > 0 && j > 0 && k > 0 && k < g.n;
-        if (!interior) {
-          finish_boundary<OP>(g, a, i, j, k, code, acc0.B, pls, base);
-        } else {
-          const double mu = c_mu[code], imu = c_inv_mu[code];
-          if (OP == OP_APPLY || OP == OP_RESID) {
-            double y[4];
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-              y[c] = ((a.blocks & BLK_A) ? mu * sA * acc0.A[c] : 0.0) + ((a.blocks & BLK_BT) ? sB * acc0.BT[c] : 0.0);
-            y[3] = ((a.blocks & BLK_B) ? sB * acc0.B : 0.0) - ((a.blocks & BLK_C) ? sC * imu * acc0.C : 0.0);
-#pragma unroll
-            for (int f = 0; f < 4; ++f) a.out[f * g.fs + o] = OP == OP_RESID ? aux[f] - y[f] : y[f];
-          } else if (OP == OP_VEL) {
-            const bool act = ((i + j + k) % a.ncolors) == a.color;
-            const double* cpl = pls[1];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              const double uc = cpl[c * FST + base];
-              double v = uc;
-              if (act) {
-                const double y = mu * sA * acc0.A[c] + sB * acc0.BT[c];
-                v = uc + (aux[c] - y) / (mu * sA * st_A[FORM][c][c][13]);
-              }
-              a.out[c * g.fs + o] = v;
-            }
-          } else if (OP == OP_P1) {
-            const double r = sB * acc0.B - sC * imu * acc0.C - aux[3];
-            a.out[o] = ((i + j + k) & 1) == 0 ? r / (sC * imu * st_C[13]) : r;
-          } else {  // P2: acc0.C holds sum_o C[o] T (including the centre)
-            const double T = pls[1][base];
-            double d = T;
-            if ((i + j + k) & 1) {
-              const double off = acc0.C - st_C[13] * T;  // neighbours only (all colour 0)
-              d = (T - sC * imu * off) / (sC * imu * st_C[13]);
-            }
-            a.out[o] = aux[3] + a.omega * d;
-          }
-        }
-      }
-      // face rows i = n, j = n (Dirichlet with an isoviscous star, else list rows)
-      if (ex_x && !(code_x & 0x80)) {
+    const double* pl = ring + s * SLOT;
+    accumulate<FORM, OP, 1>(acc0, pl, base);  // plane P is output P-1's z+1 plane
+    if (m < M - 1) {
+      accumulate<FORM, OP, 0>(acc1, pl, base);
+      accumulate<FORM, OP, -1>(acc2, pl, base);
+    }
+    const double* pls[3] = {ring + ((m + RING - 2) % RING) * SLOT, ring + ((m + RING - 1) % RING) * SLOT, pl};
+    if (!(code & (0x80 | CODE_TOP))) {
+      finish_row<FORM, OP>(g, a, i, j, k, o, code, aux, acc0, pls, base);
+    } else if (code != CODE_IRREGULAR) {
+      finish_top<FORM, OP>(g, a, i, j, k, o, code, aux, pls, base);
+    }
+    // face rows i = n, j = n (Dirichlet with an isoviscous star, else list rows)
+    if (any_ex) {
+      if (ex_x && !(cxy[0] & 0x80)) {
         const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, false>(pls, base + 1);
-        finish_boundary<OP>(g, a, g.n, j, k, code_x, Bu, pls, base + 1);
+        finish_boundary<OP>(g, a, g.n, j, k, cxy[0], Bu, pls, base + 1);
       }
-      if (ex_y && !(code_y & 0x80)) {
+      if (ex_y && !(cxy[1] & 0x80)) {
         const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<false, true>(pls, base + HX);
-        finish_boundary<OP>(g, a, i, g.n, k, code_y, Bu, pls, base + HX);
+        finish_boundary<OP>(g, a, i, g.n, k, cxy[1], Bu, pls, base + HX);
       }
-      if (ex_c && !(code_c & 0x80)) {
+      if (ex_c && !(cxy[2] & 0x80)) {
         const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, true>(pls, base + HX + 1);
-        finish_boundary<OP>(g, a, g.n, g.n, k, code_c, Bu, pls, base + HX + 1);
+        finish_boundary<OP>(g, a, g.n, g.n, k, cxy[2], Bu, pls, base + HX + 1);
       }
     }
-    __syncthreads();  // slot of plane m-2 is free for plane m+PREF
-    if (threadIdx.x == 0) issue(m + PREF);
-    acc0 = acc1;
-    acc1 = acc2;
-    acc2.zero();
+    __syncthreads();  // slot of plane m-2 is free for plane m+RING-2
+    if (threadIdx.x == 0) issue(m + RING - 2);
+    o += g.py;
+  };
+  int m = 2;
+  for (; m + 2 < M; m += 3) {
+    body(m, R2, R0, R1);
+    body(m + 1, R0, R1, R2);
+    body(m + 2, R1, R2, R0);
   }
+  if (m < M) body(m, R2, R0, R1);
+  if (m + 1 < M) body(m + 1, R0, R1, R2);
 }
 
 // ---- host side --------------------------------------------------------------
@@ -571,7 +788,22 @@ inline bool assemble_stencils(cudaStream_t st) {
   ok &= cudaMemcpyToSymbolAsync(st_B, d + off, sizeof(st_B), 0, cudaMemcpyDeviceToDevice, st) == cudaSuccess;
   off += 3 * 27;
   ok &= cudaMemcpyToSymbolAsync(st_C, d + off, sizeof(st_C), 0, cudaMemcpyDeviceToDevice, st) == cudaSuccess;
+  // the assembled stencils must equal the compile-time integer stencils the kernels use
+  std::vector<double> hst(cnt);
+  ok &= cudaMemcpyAsync(hst.data(), d, cnt * sizeof(double), cudaMemcpyDeviceToHost, st) == cudaSuccess;
   ok &= cudaStreamSynchronize(st) == cudaSuccess;
+  for (int o = 0; ok && o < 27; ++o) {
+    const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
+    for (int f = 0; f < 3; ++f)
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+          ok &= std::fabs(hst[((f * 3 + a) * 3 + b) * 27 + o] - kst(0, f, a, b, dx, dy, dz) / 6.0) <= 1e-14;
+    for (int a = 0; a < 3; ++a) {
+      ok &= std::fabs(hst[729 + a * 27 + o] - kst(1, 0, a, 0, dx, dy, dz) / 24.0) <= 1e-14;
+      ok &= std::fabs(hst[810 + a * 27 + o] - kst(2, 0, 0, a, dx, dy, dz) / 24.0) <= 1e-14;
+    }
+    ok &= std::fabs(hst[891 + o] - kst(3, 0, 0, 0, dx, dy, dz) / 6.0) <= 1e-14;
+  }
   cudaFree(d);
   done = ok;
   return ok;
@@ -586,6 +818,8 @@ inline size_t stream_smem(int op) {
 struct ListView {
   const int32_t* list;
   int n;
+  cudaStream_t side;              // list kernel runs here, concurrently (nullptr: same stream)
+  cudaEvent_t ev_fork, ev_join;
 };
 
 template <int FORM, int OP>
@@ -615,8 +849,18 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
     attr = true;
   }
   const int tiles = (g.n / TX) * (g.n / TY);
+  // z-chunks: about 4 waves of resident CTAs, at least 8 planes per chunk
   static const int kchunk_env = getenv("STK_KCHUNK") ? atoi(getenv("STK_KCHUNK")) : 0;
-  int kc = kchunk_env > 0 ? kchunk_env : 8;
+  static int slots = 0;
+  if (!slots) {
+    int per_sm = 0, nsm = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream<FORM, OP>, NT, sm);
+    slots = std::max(1, nsm * std::max(1, per_sm));
+  }
+  const int want = std::max(1, (4 * slots + tiles - 1) / tiles);
+  int kc = kchunk_env > 0 ? kchunk_env : std::max(8, (g.nzl + want - 1) / want);
   kc = std::max(1, std::min(kc, g.nzl));
   const int chunks = (g.nzl + kc - 1) / kc;
   a.kchunk = kc;
@@ -624,10 +868,20 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
   a.inP = inP;
   a.list = lv.list;
   a.nlist = lv.n;
-  a.list_blocks = (lv.n + NT - 1) / NT;
   static const int skip_list = getenv("STK_SKIP_IRR") ? atoi(getenv("STK_SKIP_IRR")) : 0;
-  a.skip_list = skip_list;
-  k_stream<FORM, OP><<<dim3(a.list_blocks + tiles * chunks), NT, sm, st>>>(mU, mP, g, a);
+  static const int fork_env = getenv("STK_LIST_FORK") ? atoi(getenv("STK_LIST_FORK")) : 0;
+  const bool do_list = lv.n > 0 && !skip_list;
+  const bool fork = do_list && fork_env && lv.side != nullptr;
+  if (fork) {
+    if (cudaEventRecord(lv.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(lv.side, lv.ev_fork, 0) != cudaSuccess)
+      return false;
+  }
+  k_stream<FORM, OP><<<dim3(tiles * chunks), NT, sm, st>>>(mU, mP, g, a);
+  if (do_list) k_list<FORM, OP><<<(lv.n + LIST_NT - 1) / LIST_NT, LIST_NT, 0, fork ? lv.side : st>>>(g, a);
+  if (fork) {
+    if (cudaEventRecord(lv.ev_join, lv.side) != cudaSuccess || cudaStreamWaitEvent(st, lv.ev_join, 0) != cudaSuccess)
+      return false;
+  }
   return true;
 }
 

@@ -88,6 +88,9 @@ struct stk_ctx {
   double* cK = nullptr;
   double* cG = nullptr;
   int* cstatus = nullptr;
+  double* d_mu = nullptr;   // per-class mu_k (256) and 1/mu_k (256)
+  cudaStream_t side = nullptr;            // list-row kernels run here, forked from `stream`
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // reductions
   double* part = nullptr;
   double* sums = nullptr;
@@ -174,6 +177,7 @@ DGrid dgrid(const stk_ctx* ctx, const Level& L) {
   g.dirmask = dirmask_of(ctx->cfg);
   g.cls = L.cls;
   g.code = L.code;
+  g.mu = ctx->d_mu;
   return g;
 }
 
@@ -226,7 +230,9 @@ void host_tables(int8_t perm[6][3], int8_t corner[8][6], int8_t choff[6][8], int
 
 // ---- level operations ------------------------------------------------------
 
-ListView lview(const Level& L) { return ListView{L.list, (int)L.nirr}; }
+ListView lview(const stk_ctx* ctx, const Level& L) {
+  return ListView{L.list, (int)L.nirr, ctx->side, ctx->ev_fork, ctx->ev_join};
+}
 
 bool use_tiled(const stk_ctx* ctx, const Level& L) {
   return ctx->kernel_mode == 1 && L.n >= 64 && !L.replicated && tiled_supported(L.n);
@@ -238,7 +244,7 @@ stk_status op_apply(stk_ctx* ctx, int l, unsigned blocks, const double* x, doubl
   DGrid g = dgrid(ctx, L);
   PScope ps(ctx, P_APPLY, l);
   if (use_tiled(ctx, L)) {
-    ST(launch_apply_tiled(ctx->cfg.form, g, lview(L), x, y, blocks, ctx->stream) ? STK_OK : STK_EUNSUP);
+    ST(launch_apply_tiled(ctx->cfg.form, g, lview(ctx, L), x, y, blocks, ctx->stream) ? STK_OK : STK_EUNSUP);
     return launched(ctx);
   }
   const unsigned nb = nblocks(owned_vertices(L));
@@ -256,7 +262,7 @@ stk_status op_residual(stk_ctx* ctx, int l, const double* x, const double* b, do
   DGrid g = dgrid(ctx, L);
   PScope ps(ctx, P_RESID, l);
   if (use_tiled(ctx, L)) {
-    ST(launch_residual_tiled(ctx->cfg.form, g, lview(L), x, b, r, ctx->stream) ? STK_OK : STK_EUNSUP);
+    ST(launch_residual_tiled(ctx->cfg.form, g, lview(ctx, L), x, b, r, ctx->stream) ? STK_OK : STK_EUNSUP);
     return launched(ctx);
   }
   const unsigned nb = nblocks(owned_vertices(L));
@@ -287,7 +293,7 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
     ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, const_cast<double*>(uin), 0, 3, L.replicated));
     PScope ps(ctx, P_VEL, l);
     if (tiled) {
-      ST(launch_vel_pass_tiled(ctx->cfg.form, g, lview(L), uin, p, b, uout, color, nc, ctx->stream) ? STK_OK
+      ST(launch_vel_pass_tiled(ctx->cfg.form, g, lview(ctx, L), uin, p, b, uout, color, nc, ctx->stream) ? STK_OK
                                                                                            : STK_EUNSUP);
     } else {
       switch (ctx->cfg.form) {
@@ -305,7 +311,7 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
   {
   PScope ps(ctx, P_P1, l);
   if (tiled) {
-    ST(launch_p_pass1_tiled(ctx->cfg.form, g, lview(L), x, gp, T, ctx->stream) ? STK_OK : STK_EUNSUP);
+    ST(launch_p_pass1_tiled(ctx->cfg.form, g, lview(ctx, L), x, gp, T, ctx->stream) ? STK_OK : STK_EUNSUP);
   } else {
     switch (ctx->cfg.form) {
       case FORM_MOD: k_p_pass1_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, x, gp, T); break;
@@ -318,7 +324,7 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
   ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, tmp, 3, 1, L.replicated));
   PScope ps2(ctx, P_P2, l);
   if (tiled) {
-    ST(launch_p_pass2_tiled(ctx->cfg.form, g, lview(L), T, p, ctx->cfg.omega, ctx->stream) ? STK_OK : STK_EUNSUP);
+    ST(launch_p_pass2_tiled(ctx->cfg.form, g, lview(ctx, L), T, p, ctx->cfg.omega, ctx->stream) ? STK_OK : STK_EUNSUP);
   } else {
     k_p_pass2_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, T, p, ctx->cfg.omega);
   }
@@ -534,32 +540,12 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
   return STK_OK;
 }
 
-const stk_ctx* g_active = nullptr;  // context whose viscosity table is in constant memory
-
-// The per-class viscosity table lives in __constant__ memory (broadcast reads);
-// with several contexts in one process, re-upload it when the caller switches.
-stk_status activate(stk_ctx* ctx) {
-  if (g_active == ctx || ctx->class_mu.empty()) return STK_OK;
-  double mu[256], imu[256];
-  for (int q = 0; q < 256; ++q) mu[q] = imu[q] = 1.0;
-  for (size_t q = 0; q < ctx->class_mu.size(); ++q) {
-    mu[q] = ctx->class_mu[q];
-    imu[q] = 1.0 / ctx->class_mu[q];
-  }
-  CK(cudaDeviceSynchronize());
-  CK(cudaMemcpyToSymbol(c_mu, mu, sizeof(mu)));
-  CK(cudaMemcpyToSymbol(c_inv_mu, imu, sizeof(imu)));
-  g_active = ctx;
-  return STK_OK;
-}
-
 stk_status check(const stk_ctx* ctx, int need_state) {
   if (!ctx) return STK_EINVAL;
   if (ctx->state < need_state) {
     const_cast<stk_ctx*>(ctx)->err = "call order violated (create -> set_viscosity -> assemble)";
     return STK_ESTATE;
   }
-  if (need_state >= 1) return activate(const_cast<stk_ctx*>(ctx));
   return STK_OK;
 }
 
@@ -669,7 +655,11 @@ stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
   if (cudaMalloc(&ctx->part, sizeof(double) * 6 * ctx->nparts) != cudaSuccess ||
       cudaMalloc(&ctx->sums, sizeof(double) * 8) != cudaSuccess ||
       cudaMallocHost(&ctx->hsums, sizeof(double) * 8) != cudaSuccess ||
-      cudaMalloc(&ctx->cstatus, sizeof(int)) != cudaSuccess) {
+      cudaMalloc(&ctx->cstatus, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_mu, sizeof(double) * 512) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     ctx->err = "allocation failed";
     return fail(STK_ENOMEM);
   }
@@ -699,8 +689,8 @@ stk_status stk_set_viscosity(stk_ctx* ctx, const uint8_t* elem_class, const doub
     imu[q] = 1.0 / class_mu[q];
   }
   ctx->class_mu.assign(class_mu, class_mu + nclass);
-  g_active = nullptr;
-  ST(activate(ctx));
+  CK(cudaMemcpyAsync(ctx->d_mu, mu, sizeof(mu), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_mu + 256, imu, sizeof(imu), cudaMemcpyHostToDevice, ctx->stream));
   Level& L = ctx->lev[0];
   const size_t ncls = (size_t)(L.cz1 - L.cz0) * L.n * L.n * 6;
   CK(cudaMemcpyAsync(L.cls, elem_class, ncls, cudaMemcpyHostToDevice, ctx->stream));
@@ -757,7 +747,10 @@ stk_status stk_assemble(stk_ctx* ctx) {
   // constant subdomain stencils for the tiled kernels
   for (int l = 0; l < ctx->nlev; ++l) {
     Level& L = ctx->lev[l];
-    if (L.n >= 64) ST(assemble_stencils(ctx->stream) ? STK_OK : STK_ECUDA);
+    if (L.n >= 64 && !assemble_stencils(ctx->stream)) {
+      ctx->err = "constant stencil assembly failed or disagrees with the compile-time stencils";
+      return STK_ECUDA;
+    }
   }
   // coarsest level: dense K (+ gauge row), Gauss-Jordan inverse
   Level& L = ctx->lev[ctx->nlev - 1];
@@ -1053,6 +1046,10 @@ stk_status stk_destroy(stk_ctx* ctx) {
   cudaFree(ctx->cK);
   cudaFree(ctx->cG);
   cudaFree(ctx->cstatus);
+  cudaFree(ctx->d_mu);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   cudaFree(ctx->part);
   cudaFree(ctx->sums);
   cudaFreeHost(ctx->hsums);
@@ -1062,7 +1059,6 @@ stk_status stk_destroy(stk_ctx* ctx) {
   cudaFree(ctx->kwork);
   cudaFree(ctx->kcoef);
   cudaFree(ctx->kpart);
-  if (g_active == ctx) g_active = nullptr;
   delete ctx;
   return STK_OK;
 }

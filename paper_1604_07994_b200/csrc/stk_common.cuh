@@ -20,9 +20,6 @@ enum { FORM_MOD = 0, FORM_SYM = 1, FORM_GRAD = 2 };
 enum { BLK_A = 1, BLK_BT = 2, BLK_B = 4, BLK_C = 8, BLK_ALL = 15 };
 constexpr uint8_t CODE_IRREGULAR = 0xFF;
 
-// per-class viscosity mu_k and 1/mu_k
-__constant__ double c_mu[256];
-__constant__ double c_inv_mu[256];
 // Kuhn permutations
 __constant__ int8_t c_perm[6][3];
 // local index (0..3) of cube corner `corner` (bit0 x, bit1 y, bit2 z) in tet t, or -1
@@ -59,7 +56,11 @@ struct DGrid {
   unsigned dirmask; // bit f set: face f is homogeneous Dirichlet
   const uint8_t* cls;   // element classes [cz - cz0][cj][ci][t]
   const uint8_t* code;  // per-vertex code (plane layout of one field)
+  const double* mu;     // per-class viscosity mu_k [0..255], 1/mu_k at mu + 256 (device)
 };
+
+__device__ __forceinline__ double mu_of(const DGrid& g, int cl) { return __ldg(g.mu + cl); }
+__device__ __forceinline__ double imu_of(const DGrid& g, int cl) { return __ldg(g.mu + 256 + cl); }
 
 __device__ __forceinline__ int64_t vidx(const DGrid& g, int i, int j, int k) {
   return (int64_t)(k - g.z0 + 1) * g.py + (int64_t)(j + 1) * g.px + (i + 1);
@@ -159,7 +160,7 @@ __device__ __forceinline__ void row_generic(const DGrid& g, int i, int j, int k,
             gm[s3] = hinv;
           }
           const uint8_t cl = elem_class(g, ci, cj, ck, t);
-          const double mu = c_mu[cl], imu = c_inv_mu[cl];
+          const double mu = mu_of(g, cl), imu = imu_of(g, cl);
           const double gg = gm[0] * gm[0] + gm[1] * gm[1] + gm[2] * gm[2];
           const double tr = G[0][0] + G[1][1] + G[2][2];
           if (blocks & BLK_A) {
@@ -189,6 +190,136 @@ __device__ __forceinline__ void row_generic(const DGrid& g, int i, int j, int k,
   if (is_dirichlet(g, i, j, k)) y[0] = y[1] = y[2] = 0.0;
 }
 
+// local cube corner (bit0 x, bit1 y, bit2 z) of vertex q = 0..3 of Kuhn tet t
+__host__ __device__ constexpr int ktet_corner(int t, int q) {
+  return q == 0 ? 0 : q == 1 ? (1 << kperm(t, 0)) : q == 2 ? ((1 << kperm(t, 0)) | (1 << kperm(t, 1))) : 7;
+}
+// is cube corner c a vertex of some tet of the cube that contains corner `own`?
+__host__ __device__ constexpr bool kcube_needs(int own, int c) {
+  bool r = false;
+  for (int t = 0; t < 6; ++t)
+    if (kcorner(own, t) >= 0 && kcorner(c, t) >= 0) r = true;
+  return r;
+}
+
+// The same row as row_generic, for rows read from global memory (the list rows
+// of the tiled kernels): the 15-point Kuhn neighbourhood (4 fields) and the
+// classes of the 24 star tets are loaded up front (one round of memory
+// latency, all loads independent), then the tets are integrated cube-major from
+// registers.  U: velocity fields 0..2 (stride fs; 0 at Dirichlet vertices and
+// outside the cube), Pf: pressure field.  PRED: pressure taken only at colour-0
+// vertices ((i+j+k) even; the masked T of the pressure Gauss-Seidel, P:1243 /
+// DESIGN R11) and no velocity.
+template <int FORM, bool PRED>
+__device__ __forceinline__ void row_list(const DGrid& g, int i, int j, int k, const double* __restrict__ U,
+                                         const double* __restrict__ Pf, unsigned blocks, double y[4], double dA[3],
+                                         double& dC) {
+  const double h = g.h, hinv = 1.0 / h;
+  const double vol = h * h * h / 6.0, vq = 0.25 * vol;
+  const double cstab = g.delta * h * h * vol;
+  const unsigned dm = g.dirmask;
+  const int n = g.n;
+  const int64_t o0 = vidx(g, i, j, k);
+  // neighbourhood values nb[o][f], o = (dz+1)*9 + (dy+1)*3 + (dx+1), Kuhn offsets only
+  double nb[27][4];
+#pragma unroll
+  for (int o = 0; o < 27; ++o) {
+    const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
+    if (!((dx >= 0 && dy >= 0 && dz >= 0) || (dx <= 0 && dy <= 0 && dz <= 0))) continue;
+    const int xi = i + dx, yj = j + dy, zk = k + dz;
+    const bool in = xi >= 0 && yj >= 0 && zk >= 0 && xi <= n && yj <= n && zk <= n;
+    const int64_t oc = o0 + dx + dy * g.px + dz * g.py;
+    if (PRED) {
+      nb[o][0] = nb[o][1] = nb[o][2] = 0.0;
+      nb[o][3] = (in && !((xi + yj + zk) & 1)) ? __ldg(Pf + oc) : 0.0;
+    } else {
+      const bool dir = !in || ((dm & 1u) && xi == 0) || ((dm & 2u) && xi == n) || ((dm & 4u) && yj == 0) ||
+                       ((dm & 8u) && yj == n) || ((dm & 16u) && zk == 0) || ((dm & 32u) && zk == n);
+#pragma unroll
+      for (int f = 0; f < 3; ++f) nb[o][f] = dir ? 0.0 : __ldg(U + f * g.fs + oc);
+      nb[o][3] = in ? __ldg(Pf + oc) : 0.0;
+    }
+  }
+  // classes of the star tets (cube own, tet t): 0xFF outside the cube
+  uint8_t cls[8][6];
+#pragma unroll
+  for (int own = 0; own < 8; ++own) {
+    const int ci = i - (own & 1), cj = j - ((own >> 1) & 1), ck = k - (own >> 2);
+    const bool in = ci >= 0 && cj >= 0 && ck >= 0 && ci < n && cj < n && ck < n;
+    const uint8_t* clp = g.cls + ((((int64_t)(ck - g.cz0)) * n + cj) * n + ci) * 6;
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      if (kcorner(own, t) < 0) continue;
+      cls[own][t] = in ? __ldg(clp + t) : (uint8_t)0xFF;
+    }
+  }
+  y[0] = y[1] = y[2] = y[3] = 0.0;
+  dA[0] = dA[1] = dA[2] = 0.0;
+  dC = 0.0;
+#pragma unroll
+  for (int own = 0; own < 8; ++own) {
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      const int m = kcorner(own, t);
+      if (m < 0) continue;
+      const int cl = cls[own][t];
+      if (cl == 0xFF) continue;
+      const int s1 = kperm(t, 0), s2 = kperm(t, 1), s3 = kperm(t, 2);
+      // neighbourhood index of tet vertex q: cube corner c relative to the vertex
+      auto vo = [&](int q) {
+        const int c = ktet_corner(t, q);
+        const int dx = (c & 1) - (own & 1), dy = ((c >> 1) & 1) - ((own >> 1) & 1), dz = (c >> 2) - (own >> 2);
+        return (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
+      };
+      const int v0 = vo(0), v1 = vo(1), v2 = vo(2), v3 = vo(3);
+      double G[3][3], gp[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        G[a][s1] = (nb[v1][a] - nb[v0][a]) * hinv;
+        G[a][s2] = (nb[v2][a] - nb[v1][a]) * hinv;
+        G[a][s3] = (nb[v3][a] - nb[v2][a]) * hinv;
+      }
+      gp[s1] = (nb[v1][3] - nb[v0][3]) * hinv;
+      gp[s2] = (nb[v2][3] - nb[v1][3]) * hinv;
+      gp[s3] = (nb[v3][3] - nb[v2][3]) * hinv;
+      double gm[3] = {0.0, 0.0, 0.0};
+      if (m == 0) {
+        gm[s1] = -hinv;
+      } else if (m == 1) {
+        gm[s1] = hinv; gm[s2] = -hinv;
+      } else if (m == 2) {
+        gm[s2] = hinv; gm[s3] = -hinv;
+      } else {
+        gm[s3] = hinv;
+      }
+      const double mu = mu_of(g, cl), imu = imu_of(g, cl);
+      const double gg = gm[0] * gm[0] + gm[1] * gm[1] + gm[2] * gm[2];
+      const double tr = G[0][0] + G[1][1] + G[2][2];
+      if (blocks & BLK_A) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          double s = G[a][0] * gm[0] + G[a][1] * gm[1] + G[a][2] * gm[2];
+          if (FORM != FORM_GRAD) s += G[0][a] * gm[0] + G[1][a] * gm[1] + G[2][a] * gm[2];
+          if (FORM == FORM_MOD) s -= tr * gm[a];
+          y[a] += mu * vol * s;
+        }
+      }
+      if (blocks & BLK_BT) {
+        const double ps = nb[v0][3] + nb[v1][3] + nb[v2][3] + nb[v3][3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) y[a] -= vq * gm[a] * ps;
+      }
+      if (blocks & BLK_B) y[3] -= vq * tr;
+      if (blocks & BLK_C) y[3] -= cstab * imu * (gm[0] * gp[0] + gm[1] * gp[1] + gm[2] * gp[2]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        dA[a] += mu * vol * (gg + (FORM == FORM_SYM ? gm[a] * gm[a] : 0.0));
+      dC += cstab * imu * gg;
+    }
+  }
+  if (is_dirichlet(g, i, j, k)) y[0] = y[1] = y[2] = 0.0;
+}
+
 // w_j = int phi_j / mu = sum_{T ni j} |T| / (4 mu_T)   (gauge weight)
 __device__ __forceinline__ double gauge_weight(const DGrid& g, int i, int j, int k) {
   const double vq = 0.25 * g.h * g.h * g.h / 6.0;
@@ -204,7 +335,7 @@ __device__ __forceinline__ double gauge_weight(const DGrid& g, int i, int j, int
         if (ci < 0 || ci >= g.n) continue;
         const int corner = (-dx) | ((-dy) << 1) | ((-dz) << 2);
         for (int t = 0; t < 6; ++t)
-          if (c_corner_m[corner][t] >= 0) w += vq * c_inv_mu[elem_class(g, ci, cj, ck, t)];
+          if (c_corner_m[corner][t] >= 0) w += vq * imu_of(g, elem_class(g, ci, cj, ck, t));
       }
     }
   }

@@ -133,17 +133,21 @@ def _star_minmax(c):
 
 def _list_rows(c, faces):
     """Expected list-row mask (R6): the star of tets inside the cube
-    holds more than one class, or the vertex lies on a traction face."""
+    holds more than one class, or the vertex lies on a traction face -- except a
+    vertex of the traction top face z = 1 that lies on no other face (its rows
+    are the truncated constant stencils of the 4 cubes below)."""
     smin, smax, _ = _star_minmax(c)
     m1 = c.shape[0] + 1
-    trac = np.zeros((m1,) * 3, bool)          # [k][j][i]
-    sl = [(slice(None), slice(None), 0), (slice(None), slice(None), -1),
-          (slice(None), 0, slice(None)), (slice(None), -1, slice(None)),
-          (0, slice(None), slice(None)), (-1, slice(None), slice(None))]
+    on = np.zeros((6,) + (m1,) * 3, bool)     # [face][k][j][i]
+    on[0][:, :, 0] = on[1][:, :, -1] = True
+    on[2][:, 0, :] = on[3][:, -1, :] = True
+    on[4][0] = on[5][-1] = True
+    trac = np.zeros((m1,) * 3, bool)
     for f in range(6):
         if int(faces[f]) == 1:
-            trac[sl[f]] = True
-    return (smin != smax) | trac
+            trac |= on[f]
+    top_only = on[5] & (on.sum(axis=0) == 1) & (int(faces[5]) == 1)
+    return (smin != smax) | (trac & ~top_only)
 
 
 @pytest.mark.parametrize("cfgname", ["cfg4", "cfg2"])
