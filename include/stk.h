@@ -177,11 +177,14 @@ stk_status stk_set_kernel_mode(stk_ctx* ctx, int32_t mode);
 /* Number of kernels this context launched so far (evidence counter). */
 int64_t stk_launch_count(const stk_ctx* ctx);
 
-/* Event-timed kernel profile.  While enabled, every op brackets its kernel
- * launches with CUDA events on cfg.stream.  stk_profile_read sums the records of
+/* Event-timed kernel profile.  on = 1: every op brackets its kernel launches
+ * with CUDA events on cfg.stream, except that the V-cycle levels >= 1 run as
+ * one captured CUDA graph timed as op 10; on = 2: the graph is bypassed and
+ * every launch is timed; on = 0: off.  stk_profile_read sums the records of
  * one op (0 apply, 1 residual, 2 velocity colour pass, 3 pressure pass 1,
  * 4 pressure pass 2, 5 restriction, 6 prolongation, 7 coarse solve,
- * 8 reductions, 9 Krylov vector ops) on one level (-1 = all); synchronises. */
+ * 8 reductions, 9 Krylov vector ops, 10 coarse-level graph) on one level
+ * (-1 = all); synchronises.  STK_EINVAL for on outside 0..2. */
 stk_status stk_profile_enable(stk_ctx* ctx, int32_t on);
 stk_status stk_profile_reset(stk_ctx* ctx);
 stk_status stk_profile_read(stk_ctx* ctx, int32_t op, int32_t level, int64_t* launches, double* ms);

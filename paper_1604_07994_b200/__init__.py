@@ -207,9 +207,11 @@ class StokesContext:
         return _lib.stk_launch_count(self.h)
 
     PROFILE_OPS = ("apply", "residual", "vel_pass", "p_pass1", "p_pass2", "restrict", "prolong",
-                   "coarse", "reduce", "krylov")
+                   "coarse", "reduce", "krylov", "coarse_graph")
 
-    def profile(self, on: bool = True):
+    def profile(self, on=True):
+        """Event-time every launch: True/1 (the coarse-level CUDA graph timed as one
+        op, 'coarse_graph'), 2 (every launch, graph disabled), False/0 off."""
         self._chk("stk_profile_enable", _lib.stk_profile_enable(self.h, int(on)))
 
     def profile_reset(self):

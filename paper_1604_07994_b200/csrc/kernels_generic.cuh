@@ -1,5 +1,5 @@
 // Generic (element-row) kernels: one thread per owned vertex, every row by
-// the element loop of row_generic.  Used on the small levels (n < 64) and as
+// the element loop (row_list: neighbourhood gathered up front).  Used on the small levels (n < 64) and as
 // the reference device path for the tiled constant-stencil kernels.
 #pragma once
 #include "stk_common.cuh"
@@ -22,9 +22,8 @@ __global__ void k_apply_generic(DGrid g, const double* __restrict__ x, double* _
                                 unsigned blocks) {
   int i, j, k;
   if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
-  FetchVec fx{x, x + 3 * g.fs};
   double r[4], dA[3], dC;
-  row_generic<FORM>(g, i, j, k, fx, blocks, r, dA, dC);
+  row_list<FORM, false>(g, i, j, k, x, x + 3 * g.fs, blocks, r, dA, dC);
   const int64_t o = vidx(g, i, j, k);
 #pragma unroll
   for (int f = 0; f < 4; ++f) y[f * g.fs + o] = r[f];
@@ -36,9 +35,8 @@ __global__ void k_residual_generic(DGrid g, const double* __restrict__ x,
                                    const double* __restrict__ b, double* __restrict__ r) {
   int i, j, k;
   if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
-  FetchVec fx{x, x + 3 * g.fs};
   double y[4], dA[3], dC;
-  row_generic<FORM>(g, i, j, k, fx, BLK_ALL, y, dA, dC);
+  row_list<FORM, false>(g, i, j, k, x, x + 3 * g.fs, BLK_ALL, y, dA, dC);
   const int64_t o = vidx(g, i, j, k);
   const bool dir = is_dirichlet(g, i, j, k);
 #pragma unroll
@@ -61,9 +59,8 @@ __global__ void k_vel_pass_generic(DGrid g, const double* __restrict__ uin,
     for (int a = 0; a < 3; ++a) uout[a * g.fs + o] = is_dirichlet(g, i, j, k) ? 0.0 : uin[a * g.fs + o];
     return;
   }
-  FetchVec fx{uin, p};
   double y[4], dA[3], dC;
-  row_generic<FORM>(g, i, j, k, fx, BLK_A | BLK_BT, y, dA, dC);
+  row_list<FORM, false>(g, i, j, k, uin, p, BLK_A | BLK_BT, y, dA, dC);
 #pragma unroll
   for (int a = 0; a < 3; ++a) uout[a * g.fs + o] = uin[a * g.fs + o] + (b[a * g.fs + o] - y[a]) / dA[a];
 }
@@ -74,22 +71,12 @@ __global__ void k_p_pass1_generic(DGrid g, const double* __restrict__ x,
                                   const double* __restrict__ gp, double* __restrict__ T) {
   int i, j, k;
   if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
-  FetchVec fx{x, x + 3 * g.fs};
   double y[4], dA[3], dC;
-  row_generic<FORM>(g, i, j, k, fx, BLK_B | BLK_C, y, dA, dC);
+  row_list<FORM, false>(g, i, j, k, x, x + 3 * g.fs, BLK_B | BLK_C, y, dA, dC);
   const int64_t o = vidx(g, i, j, k);
   const double r = y[3] - gp[o];
   T[o] = ((i + j + k) & 1) == 0 ? r / dC : r;
 }
-
-// masked fetch: pressure = T at colour-0 vertices, 0 elsewhere; velocity 0
-struct FetchRedP {
-  const double* __restrict__ T;
-  __device__ __forceinline__ double operator()(const DGrid& g, int i, int j, int k, int f) const {
-    if (f != 3 || ((i + j + k) & 1)) return 0.0;
-    return T[vidx(g, i, j, k)];
-  }
-};
 
 // Pressure step, part 2: delta_1 = (r_p - C delta_0)/C_ii on colour 1,
 // delta_0 = T on colour 0;  p += omega * delta
@@ -103,9 +90,8 @@ __global__ void k_p_pass2_generic(DGrid g, const double* __restrict__ T, double*
   if (((i + j + k) & 1) == 0) {
     d = T[o];
   } else {
-    FetchRedP fx{T};
     double y[4], dA[3], dC;
-    row_generic<FORM>(g, i, j, k, fx, BLK_C, y, dA, dC);
+    row_list<FORM, true>(g, i, j, k, nullptr, T, BLK_C, y, dA, dC);
     d = (T[o] + y[3]) / dC;   // y[3] = -(C delta_0)_i
   }
   p[o] += omega * d;
@@ -533,6 +519,213 @@ __global__ void k_coarse_apply(DGrid g, const int32_t* __restrict__ dofs, int N,
     const int f = (d >> 28) & 0xF, k = (d >> 18) & 0x3FF, j = (d >> 9) & 0x1FF, i = d & 0x1FF;
     x[f * g.fs + vidx(g, i, j, k)] = s;
   }
+}
+
+
+// ---- warp-per-row kernels for the small levels (n <= 32) --------------------
+// With few rows per level the kernel time is the latency of one row, so a row
+// is spread over a warp: lane l < 24 integrates tet l of the star.
+
+// star tets of a vertex, lane -> own corner | tet << 3 (own corners 0..7 in
+// order, tets 0..5 in order), packed 6 bits per lane at compile time
+__host__ __device__ constexpr int kstar_entry(int l) {
+  int cnt = 0;
+  for (int own = 0; own < 8; ++own)
+    for (int t = 0; t < 6; ++t)
+      if (kcorner(own, t) >= 0) {
+        if (cnt == l) return own | (t << 3);
+        ++cnt;
+      }
+  return 0;
+}
+__host__ __device__ constexpr uint64_t kstar_pack(int w) {
+  uint64_t v = 0;
+  for (int q = 0; q < 8; ++q) v |= (uint64_t)kstar_entry(8 * w + q) << (8 * q);
+  return v;
+}
+constexpr uint64_t KSTAR0 = kstar_pack(0), KSTAR1 = kstar_pack(1), KSTAR2 = kstar_pack(2);
+static_assert(kstar_entry(23) == (7 | (5 << 3)), "24 star tets");
+
+// The row of row_generic at (i,j,k), one warp: lane l < 24 integrates star tet
+// l from global memory, a butterfly reduction gives all lanes y[4], dA[3], dC.
+template <int FORM, bool PRED>
+__device__ __forceinline__ void row_warp(const DGrid& g, int i, int j, int k, const double* __restrict__ U,
+                                         const double* __restrict__ Pf, unsigned blocks, double y[4], double dA[3],
+                                         double& dC) {
+  const int lane = threadIdx.x & 31;
+  double r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int n = g.n;
+  if (lane < 24) {
+    const uint64_t w = lane < 8 ? KSTAR0 : lane < 16 ? KSTAR1 : KSTAR2;
+    const int e = (int)((w >> (8 * (lane & 7))) & 0xFF);
+    const int own = e & 7, t = e >> 3;
+    const int ci = i - (own & 1), cj = j - ((own >> 1) & 1), ck = k - (own >> 2);
+    if (ci >= 0 && cj >= 0 && ck >= 0 && ci < n && cj < n && ck < n) {
+      const double h = g.h, hinv = 1.0 / h;
+      const double vol = h * h * h / 6.0, vq = 0.25 * vol;
+      const double cstab = g.delta * h * h * vol;
+      const unsigned dm = g.dirmask;
+      const int s1 = kperm(t, 0), s2 = kperm(t, 1), s3 = kperm(t, 2);
+      const int m = kcorner(own, t);
+      const int cl = g.cls[((((int64_t)(ck - g.cz0)) * n + cj) * n + ci) * 6 + t];
+      double val[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = ktet_corner(t, q);
+        const int xi = ci + (c & 1), yj = cj + ((c >> 1) & 1), zk = ck + (c >> 2);
+        const int64_t oc = vidx(g, xi, yj, zk);
+        if (PRED) {
+          val[q][0] = val[q][1] = val[q][2] = 0.0;
+          val[q][3] = ((xi + yj + zk) & 1) ? 0.0 : __ldg(Pf + oc);
+        } else {
+          const bool dir = ((dm & 1u) && xi == 0) || ((dm & 2u) && xi == n) || ((dm & 4u) && yj == 0) ||
+                           ((dm & 8u) && yj == n) || ((dm & 16u) && zk == 0) || ((dm & 32u) && zk == n);
+#pragma unroll
+          for (int f = 0; f < 3; ++f) val[q][f] = dir ? 0.0 : __ldg(U + f * g.fs + oc);
+          val[q][3] = __ldg(Pf + oc);
+        }
+      }
+      double G[3][3], gp[3], gm[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double d1 = (val[1][a] - val[0][a]) * hinv, d2 = (val[2][a] - val[1][a]) * hinv,
+                     d3 = (val[3][a] - val[2][a]) * hinv;
+        G[a][0] = s1 == 0 ? d1 : s2 == 0 ? d2 : d3;
+        G[a][1] = s1 == 1 ? d1 : s2 == 1 ? d2 : d3;
+        G[a][2] = s1 == 2 ? d1 : s2 == 2 ? d2 : d3;
+      }
+      {
+        const double d1 = (val[1][3] - val[0][3]) * hinv, d2 = (val[2][3] - val[1][3]) * hinv,
+                     d3 = (val[3][3] - val[2][3]) * hinv;
+        gp[0] = s1 == 0 ? d1 : s2 == 0 ? d2 : d3;
+        gp[1] = s1 == 1 ? d1 : s2 == 1 ? d2 : d3;
+        gp[2] = s1 == 2 ? d1 : s2 == 2 ? d2 : d3;
+      }
+      // grad lambda_m: -e_s1 (m=0), e_s1 - e_s2 (1), e_s2 - e_s3 (2), e_s3 (3), over h
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        double v;
+        if (m == 0) v = (d == s1) ? -hinv : 0.0;
+        else if (m == 1) v = (d == s1) ? hinv : (d == s2) ? -hinv : 0.0;
+        else if (m == 2) v = (d == s2) ? hinv : (d == s3) ? -hinv : 0.0;
+        else v = (d == s3) ? hinv : 0.0;
+        gm[d] = v;
+      }
+      const double mu = mu_of(g, cl), imu = imu_of(g, cl);
+      const double gg = gm[0] * gm[0] + gm[1] * gm[1] + gm[2] * gm[2];
+      const double tr = G[0][0] + G[1][1] + G[2][2];
+      if (blocks & BLK_A) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          double sv = G[a][0] * gm[0] + G[a][1] * gm[1] + G[a][2] * gm[2];
+          if (FORM != FORM_GRAD) sv += G[0][a] * gm[0] + G[1][a] * gm[1] + G[2][a] * gm[2];
+          if (FORM == FORM_MOD) sv -= tr * gm[a];
+          r[a] += mu * vol * sv;
+        }
+      }
+      if (blocks & BLK_BT) {
+        const double ps = val[0][3] + val[1][3] + val[2][3] + val[3][3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) r[a] -= vq * gm[a] * ps;
+      }
+      if (blocks & BLK_B) r[3] -= vq * tr;
+      if (blocks & BLK_C) r[3] -= cstab * imu * (gm[0] * gp[0] + gm[1] * gp[1] + gm[2] * gp[2]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) r[4 + a] = mu * vol * (gg + (FORM == FORM_SYM ? gm[a] * gm[a] : 0.0));
+      r[7] = cstab * imu * gg;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r[q] += __shfl_xor_sync(0xffffffffu, r[q], off);
+  y[0] = r[0]; y[1] = r[1]; y[2] = r[2]; y[3] = r[3];
+  dA[0] = r[4]; dA[1] = r[5]; dA[2] = r[6];
+  dC = r[7];
+  if (is_dirichlet(g, i, j, k)) y[0] = y[1] = y[2] = 0.0;
+}
+
+constexpr int GW_NT = 128;  // 4 rows per CTA
+__device__ __forceinline__ bool warp_vertex(const DGrid& g, int& i, int& j, int& k) {
+  return owned_vertex(g, (blockIdx.x * (int64_t)GW_NT + threadIdx.x) >> 5, i, j, k);
+}
+
+template <int FORM>
+__global__ void __launch_bounds__(GW_NT) k_apply_gw(DGrid g, const double* __restrict__ x, double* __restrict__ y,
+                                                    unsigned blocks) {
+  int i, j, k;
+  if (!warp_vertex(g, i, j, k)) return;
+  double r[4], dA[3], dC;
+  row_warp<FORM, false>(g, i, j, k, x, x + 3 * g.fs, blocks, r, dA, dC);
+  if ((threadIdx.x & 31) == 0) {
+    const int64_t o = vidx(g, i, j, k);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) y[f * g.fs + o] = r[f];
+  }
+}
+
+template <int FORM>
+__global__ void __launch_bounds__(GW_NT) k_residual_gw(DGrid g, const double* __restrict__ x,
+                                                       const double* __restrict__ b, double* __restrict__ r) {
+  int i, j, k;
+  if (!warp_vertex(g, i, j, k)) return;
+  double y[4], dA[3], dC;
+  row_warp<FORM, false>(g, i, j, k, x, x + 3 * g.fs, BLK_ALL, y, dA, dC);
+  if ((threadIdx.x & 31) == 0) {
+    const int64_t o = vidx(g, i, j, k);
+    const bool dir = is_dirichlet(g, i, j, k);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) r[f * g.fs + o] = (f < 3 && dir) ? 0.0 : b[f * g.fs + o] - y[f];
+  }
+}
+
+template <int FORM>
+__global__ void __launch_bounds__(GW_NT) k_vel_pass_gw(DGrid g, const double* __restrict__ uin,
+                                                       const double* __restrict__ p, const double* __restrict__ b,
+                                                       double* __restrict__ uout, int color, int ncolors) {
+  int i, j, k;
+  if (!warp_vertex(g, i, j, k)) return;
+  const int64_t o = vidx(g, i, j, k);
+  const bool dir = is_dirichlet(g, i, j, k);
+  const bool active = ((i + j + k) % ncolors == color) && !dir;  // warp-uniform
+  double y[4], dA[3], dC;
+  if (active) row_warp<FORM, false>(g, i, j, k, uin, p, BLK_A | BLK_BT, y, dA, dC);
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      uout[a * g.fs + o] = dir ? 0.0 : active ? uin[a * g.fs + o] + (b[a * g.fs + o] - y[a]) / dA[a] : uin[a * g.fs + o];
+  }
+}
+
+template <int FORM>
+__global__ void __launch_bounds__(GW_NT) k_p_pass1_gw(DGrid g, const double* __restrict__ x,
+                                                      const double* __restrict__ gp, double* __restrict__ T) {
+  int i, j, k;
+  if (!warp_vertex(g, i, j, k)) return;
+  double y[4], dA[3], dC;
+  row_warp<FORM, false>(g, i, j, k, x, x + 3 * g.fs, BLK_B | BLK_C, y, dA, dC);
+  if ((threadIdx.x & 31) == 0) {
+    const int64_t o = vidx(g, i, j, k);
+    const double r = y[3] - gp[o];
+    T[o] = ((i + j + k) & 1) == 0 ? r / dC : r;
+  }
+}
+
+template <int FORM>
+__global__ void __launch_bounds__(GW_NT) k_p_pass2_gw(DGrid g, const double* __restrict__ T, double* __restrict__ p,
+                                                      double omega) {
+  int i, j, k;
+  if (!warp_vertex(g, i, j, k)) return;
+  const int64_t o = vidx(g, i, j, k);
+  double d = 0.0;
+  if (((i + j + k) & 1) == 0) {
+    d = T[o];
+  } else {
+    double y[4], dA[3], dC;
+    row_warp<FORM, true>(g, i, j, k, nullptr, T, BLK_C, y, dA, dC);
+    d = (T[o] + y[3]) / dC;
+  }
+  if ((threadIdx.x & 31) == 0) p[o] += omega * d;
 }
 
 }  // namespace stk

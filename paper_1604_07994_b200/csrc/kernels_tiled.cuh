@@ -5,8 +5,8 @@
 //    touching both kinds of faces) are evaluated by a second kernel, k_list:
 //    one row per thread by the cube-major element loop row_list (exact element
 //    formulas), reading the input from global memory (L2).  The two kernels
-//    write disjoint rows; k_list runs after k_stream on the same stream (or
-//    concurrently on a forked side stream, STK_LIST_FORK=1).
+//    write disjoint rows; k_list runs concurrently on a side stream forked from
+//    (and joined back into) the caller's stream (STK_LIST_FORK=0: serial).
 //  * A stream CTA owns a TX x TY column tile (i in [i0, i0+TX), j in
 //    [j0, j0+TY), i0+TX <= n) and a chunk of z-planes.  Each plane of the input
 //    fields, with a 1-vertex xy halo, is staged in shared memory by TMA boxes
@@ -849,7 +849,7 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
     attr = true;
   }
   const int tiles = (g.n / TX) * (g.n / TY);
-  // z-chunks: about 4 waves of resident CTAs, at least 8 planes per chunk
+  // z-chunks: about 4 waves of resident CTAs, 4..32 planes per chunk
   static const int kchunk_env = getenv("STK_KCHUNK") ? atoi(getenv("STK_KCHUNK")) : 0;
   static int slots = 0;
   if (!slots) {
@@ -860,7 +860,9 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
     slots = std::max(1, nsm * std::max(1, per_sm));
   }
   const int want = std::max(1, (4 * slots + tiles - 1) / tiles);
-  int kc = kchunk_env > 0 ? kchunk_env : std::max(8, (g.nzl + want - 1) / want);
+  // (chunks of <= 32 planes keep concurrently streaming neighbour tiles at the
+  // same height, so their halo planes are shared through L2)
+  int kc = kchunk_env > 0 ? kchunk_env : std::min(32, std::max(4, (g.nzl + want - 1) / want));
   kc = std::max(1, std::min(kc, g.nzl));
   const int chunks = (g.nzl + kc - 1) / kc;
   a.kchunk = kc;
@@ -869,7 +871,7 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
   a.list = lv.list;
   a.nlist = lv.n;
   static const int skip_list = getenv("STK_SKIP_IRR") ? atoi(getenv("STK_SKIP_IRR")) : 0;
-  static const int fork_env = getenv("STK_LIST_FORK") ? atoi(getenv("STK_LIST_FORK")) : 0;
+  static const int fork_env = getenv("STK_LIST_FORK") ? atoi(getenv("STK_LIST_FORK")) : 1;
   const bool do_list = lv.n > 0 && !skip_list;
   const bool fork = do_list && fork_env && lv.side != nullptr;
   if (fork) {

@@ -37,13 +37,13 @@ struct Level {
 };
 
 // event-timed profile of the kernels launched while enabled (stk_profile_*)
-enum { P_APPLY = 0, P_RESID, P_VEL, P_P1, P_P2, P_RESTRICT, P_PROLONG, P_COARSE, P_REDUCE, P_KRYLOV, P_NOPS };
+enum { P_APPLY = 0, P_RESID, P_VEL, P_P1, P_P2, P_RESTRICT, P_PROLONG, P_COARSE, P_REDUCE, P_KRYLOV, P_CGRAPH, P_NOPS };
 struct ProfRec {
   int op, level;
   cudaEvent_t e0, e1;
 };
 struct Prof {
-  bool on = false;
+  int on = 0;  // 1: per-launch events except inside the coarse graph (timed as one op); 2: no graph
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
   cudaEvent_t get() {
@@ -90,6 +90,9 @@ struct stk_ctx {
   int* cstatus = nullptr;
   double* d_mu = nullptr;   // per-class mu_k (256) and 1/mu_k (256)
   cudaStream_t side = nullptr;            // list-row kernels run here, forked from `stream`
+  cudaStream_t cap = nullptr;             // capture stream for the coarse-level CUDA graph
+  cudaGraphExec_t coarse_exec = nullptr;  // levels >= 1 of the V-cycle (fixed internal buffers)
+  int64_t coarse_launches = 0;            // kernels in that graph (launch accounting)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // reductions
   double* part = nullptr;
@@ -183,6 +186,9 @@ DGrid dgrid(const stk_ctx* ctx, const Level& L) {
 
 int64_t owned_vertices(const Level& L) { return (int64_t)(L.n + 1) * (L.n + 1) * L.nzl; }
 unsigned nblocks(int64_t work) { return (unsigned)((work + kThreads - 1) / kThreads); }
+// small levels (n <= 16): one warp per row (latency-bound; kernels_generic.cuh *_gw)
+bool warp_rows(const Level& L) { return L.n <= 16; }
+unsigned nblocks_gw(const Level& L) { return (unsigned)((owned_vertices(L) * 32 + GW_NT - 1) / GW_NT); }
 
 bool has_traction(const stk_config& c) {
   for (int f = 0; f < 6; ++f)
@@ -247,6 +253,15 @@ stk_status op_apply(stk_ctx* ctx, int l, unsigned blocks, const double* x, doubl
     ST(launch_apply_tiled(ctx->cfg.form, g, lview(ctx, L), x, y, blocks, ctx->stream) ? STK_OK : STK_EUNSUP);
     return launched(ctx);
   }
+  if (warp_rows(L)) {
+    const unsigned nw = nblocks_gw(L);
+    switch (ctx->cfg.form) {
+      case FORM_MOD: k_apply_gw<FORM_MOD><<<nw, GW_NT, 0, ctx->stream>>>(g, x, y, blocks); break;
+      case FORM_SYM: k_apply_gw<FORM_SYM><<<nw, GW_NT, 0, ctx->stream>>>(g, x, y, blocks); break;
+      default: k_apply_gw<FORM_GRAD><<<nw, GW_NT, 0, ctx->stream>>>(g, x, y, blocks); break;
+    }
+    return launched(ctx);
+  }
   const unsigned nb = nblocks(owned_vertices(L));
   switch (ctx->cfg.form) {
     case FORM_MOD: k_apply_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, x, y, blocks); break;
@@ -263,6 +278,15 @@ stk_status op_residual(stk_ctx* ctx, int l, const double* x, const double* b, do
   PScope ps(ctx, P_RESID, l);
   if (use_tiled(ctx, L)) {
     ST(launch_residual_tiled(ctx->cfg.form, g, lview(ctx, L), x, b, r, ctx->stream) ? STK_OK : STK_EUNSUP);
+    return launched(ctx);
+  }
+  if (warp_rows(L)) {
+    const unsigned nw = nblocks_gw(L);
+    switch (ctx->cfg.form) {
+      case FORM_MOD: k_residual_gw<FORM_MOD><<<nw, GW_NT, 0, ctx->stream>>>(g, x, b, r); break;
+      case FORM_SYM: k_residual_gw<FORM_SYM><<<nw, GW_NT, 0, ctx->stream>>>(g, x, b, r); break;
+      default: k_residual_gw<FORM_GRAD><<<nw, GW_NT, 0, ctx->stream>>>(g, x, b, r); break;
+    }
     return launched(ctx);
   }
   const unsigned nb = nblocks(owned_vertices(L));
@@ -295,6 +319,13 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
     if (tiled) {
       ST(launch_vel_pass_tiled(ctx->cfg.form, g, lview(ctx, L), uin, p, b, uout, color, nc, ctx->stream) ? STK_OK
                                                                                            : STK_EUNSUP);
+    } else if (warp_rows(L)) {
+      const unsigned nw = nblocks_gw(L);
+      switch (ctx->cfg.form) {
+        case FORM_MOD: k_vel_pass_gw<FORM_MOD><<<nw, GW_NT, 0, ctx->stream>>>(g, uin, p, b, uout, color, nc); break;
+        case FORM_SYM: k_vel_pass_gw<FORM_SYM><<<nw, GW_NT, 0, ctx->stream>>>(g, uin, p, b, uout, color, nc); break;
+        default: k_vel_pass_gw<FORM_GRAD><<<nw, GW_NT, 0, ctx->stream>>>(g, uin, p, b, uout, color, nc); break;
+      }
     } else {
       switch (ctx->cfg.form) {
         case FORM_MOD: k_vel_pass_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, uin, p, b, uout, color, nc); break;
@@ -312,6 +343,13 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
   PScope ps(ctx, P_P1, l);
   if (tiled) {
     ST(launch_p_pass1_tiled(ctx->cfg.form, g, lview(ctx, L), x, gp, T, ctx->stream) ? STK_OK : STK_EUNSUP);
+  } else if (warp_rows(L)) {
+    const unsigned nw = nblocks_gw(L);
+    switch (ctx->cfg.form) {
+      case FORM_MOD: k_p_pass1_gw<FORM_MOD><<<nw, GW_NT, 0, ctx->stream>>>(g, x, gp, T); break;
+      case FORM_SYM: k_p_pass1_gw<FORM_SYM><<<nw, GW_NT, 0, ctx->stream>>>(g, x, gp, T); break;
+      default: k_p_pass1_gw<FORM_GRAD><<<nw, GW_NT, 0, ctx->stream>>>(g, x, gp, T); break;
+    }
   } else {
     switch (ctx->cfg.form) {
       case FORM_MOD: k_p_pass1_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, x, gp, T); break;
@@ -325,6 +363,8 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
   PScope ps2(ctx, P_P2, l);
   if (tiled) {
     ST(launch_p_pass2_tiled(ctx->cfg.form, g, lview(ctx, L), T, p, ctx->cfg.omega, ctx->stream) ? STK_OK : STK_EUNSUP);
+  } else if (warp_rows(L)) {
+    k_p_pass2_gw<FORM_MOD><<<nblocks_gw(L), GW_NT, 0, ctx->stream>>>(g, T, p, ctx->cfg.omega);
   } else {
     k_p_pass2_generic<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, T, p, ctx->cfg.omega);
   }
@@ -386,6 +426,56 @@ stk_status op_gauge(stk_ctx* ctx, int l, double* x) {
   return launched(ctx);
 }
 
+stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x);
+
+// lev[1].x = V-cycle of levels >= 1 on lev[1].b from a zero guess.  These
+// levels only touch context-owned buffers, so the whole sequence (a few hundred
+// small launches with the V_var schedule) is captured once into a CUDA graph
+// and replayed; the graph is rebuilt after every stk_assemble.
+stk_status op_coarse_part(stk_ctx* ctx) {
+  Level& C = ctx->lev[1];
+  static const bool no_graph = getenv("STK_NO_GRAPH") && atoi(getenv("STK_NO_GRAPH"));
+  if (ctx->prof.on == 2 || no_graph) {
+    CK(cudaMemsetAsync(C.x, 0, sizeof(double) * C.vlen, ctx->stream));
+    return op_vcycle(ctx, 1, C.b, C.x);
+  }
+  if (!ctx->coarse_exec) {
+    const int prof_saved = ctx->prof.on;
+    ctx->prof.on = 0;  // no timing events inside the captured graph
+    cudaStream_t saved = ctx->stream;
+    ctx->stream = ctx->cap;
+    CK(cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeRelaxed));
+    const int64_t l0 = ctx->launches;
+    stk_status s = STK_OK;
+    if (cudaMemsetAsync(C.x, 0, sizeof(double) * C.vlen, ctx->cap) != cudaSuccess) s = STK_ECUDA;
+    if (s == STK_OK) s = op_vcycle(ctx, 1, C.b, C.x);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(ctx->cap, &graph);
+    ctx->stream = saved;
+    ctx->prof.on = prof_saved;
+    ctx->coarse_launches = ctx->launches - l0;  // counted when the graph is launched
+    ctx->launches = l0;
+    if (s != STK_OK) return s;
+    if (e != cudaSuccess) {
+      ctx->err = std::string("coarse graph capture: ") + cudaGetErrorString(e);
+      return STK_ECUDA;
+    }
+    const cudaError_t ei = cudaGraphInstantiate(&ctx->coarse_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+      ctx->coarse_exec = nullptr;
+      ctx->err = std::string("coarse graph instantiate: ") + cudaGetErrorString(ei);
+      return STK_ECUDA;
+    }
+  }
+  {
+    PScope ps(ctx, P_CGRAPH, 1);
+    CK(cudaGraphLaunch(ctx->coarse_exec, ctx->stream));
+  }
+  ctx->launches += ctx->coarse_launches;
+  return STK_OK;
+}
+
 stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x) {
   if (l == ctx->nlev - 1) return op_coarse(ctx, b, x);
   Level& L = ctx->lev[l];
@@ -395,8 +485,12 @@ stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x) {
   for (int s = 0; s < nu_pre; ++s) ST(op_uzawa(ctx, l, x, b));
   ST(op_residual(ctx, l, x, b, L.r));
   ST(op_restrict(ctx, l, L.r, C.b));
-  CK(cudaMemsetAsync(C.x, 0, sizeof(double) * C.vlen, ctx->stream));
-  ST(op_vcycle(ctx, l + 1, C.b, C.x));
+  if (l == 0) {
+    ST(op_coarse_part(ctx));
+  } else {
+    CK(cudaMemsetAsync(C.x, 0, sizeof(double) * C.vlen, ctx->stream));
+    ST(op_vcycle(ctx, l + 1, C.b, C.x));
+  }
   ST(op_prolong_add(ctx, l + 1, C.x, x));
   for (int s = 0; s < nu_post; ++s) ST(op_uzawa(ctx, l, x, b));
   return STK_OK;
@@ -540,6 +634,11 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
   return STK_OK;
 }
 
+void drop_graphs(stk_ctx* ctx) {
+  if (ctx->coarse_exec) cudaGraphExecDestroy(ctx->coarse_exec);
+  ctx->coarse_exec = nullptr;
+}
+
 stk_status check(const stk_ctx* ctx, int need_state) {
   if (!ctx) return STK_EINVAL;
   if (ctx->state < need_state) {
@@ -658,6 +757,7 @@ stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
       cudaMalloc(&ctx->cstatus, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&ctx->d_mu, sizeof(double) * 512) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     ctx->err = "allocation failed";
@@ -702,6 +802,7 @@ stk_status stk_set_viscosity(stk_ctx* ctx, const uint8_t* elem_class, const doub
 
 stk_status stk_assemble(stk_ctx* ctx) {
   ST(check(ctx, 1));
+  drop_graphs(ctx);
   // coarse classes
   for (int l = 1; l < ctx->nlev; ++l) {
     Level& F = ctx->lev[l - 1];
@@ -995,6 +1096,7 @@ stk_status stk_solve(stk_ctx* ctx, const double* b, double* x, double rtol, int3
 stk_status stk_set_kernel_mode(stk_ctx* ctx, int32_t mode) {
   if (!ctx || (mode != 0 && mode != 1)) return STK_EINVAL;
   ctx->kernel_mode = mode;
+  drop_graphs(ctx);
   return STK_OK;
 }
 
@@ -1002,7 +1104,8 @@ int64_t stk_launch_count(const stk_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 stk_status stk_profile_enable(stk_ctx* ctx, int32_t on) {
   if (!ctx) return STK_EINVAL;
-  ctx->prof.on = on != 0;
+  if (on < 0 || on > 2) return STK_EINVAL;
+  ctx->prof.on = on;
   return STK_OK;
 }
 
@@ -1050,6 +1153,8 @@ stk_status stk_destroy(stk_ctx* ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  drop_graphs(ctx);
+  if (ctx->cap) cudaStreamDestroy(ctx->cap);
   cudaFree(ctx->part);
   cudaFree(ctx->sums);
   cudaFreeHost(ctx->hsums);

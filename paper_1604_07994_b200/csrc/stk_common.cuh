@@ -79,18 +79,6 @@ __device__ __forceinline__ uint8_t elem_class(const DGrid& g, int ci, int cj, in
   return g.cls[((((int64_t)(ck - g.cz0)) * g.n + cj) * g.n + ci) * 6 + t];
 }
 
-// Fetch functor: 4-field vector in the level layout, velocity masked at Dirichlet.
-struct FetchVec {
-  const double* __restrict__ u;  // base of fields 0..2 (stride fs)
-  const double* __restrict__ p;  // pressure field base
-  __device__ __forceinline__ double operator()(const DGrid& g, int i, int j, int k, int f) const {
-    const int64_t o = vidx(g, i, j, k);
-    if (f == 3) return p[o];
-    if (is_dirichlet(g, i, j, k)) return 0.0;
-    return u[f * g.fs + o];
-  }
-};
-
 // Generic row of K = [[A, B^T], [B, -C]] at owned vertex (i,j,k), by the
 // element loop over its 24 incident tetrahedra (exact P1 integration):
 //   (A u)_{i,a} = sum_T mu_T |T| [(G + G^T - tr(G) I) g_m]_a      (mod)
