@@ -45,6 +45,12 @@ constexpr int HX = TX + 2, HY = TY + 2, PLANE = HX * HY;
 // shared-memory stride of one staged field plane: 128-byte aligned TMA destinations
 constexpr int FST = ((PLANE + 15) / 16) * 16;
 constexpr int PREF = 3, RING = PREF + 2;
+// per-row auxiliary fields, prefetched one row ahead by cp.async into a per-thread
+// double buffer: RESID b (4), VEL f (3), P1 g (1), P2 own p (1)
+__host__ __device__ constexpr int n_aux(int op) { return op == 1 ? 4 : op == 2 ? 3 : (op == 3 || op == 4) ? 1 : 0; }
+// doubles per ring slot: staged fields (with halo)
+__host__ __device__ constexpr int slot_doubles(int op) { return (op == 4 ? 1 : 4) * FST; }
+
 
 // Integer unit stencils of an interior vertex (h = 1, mu = 1, delta = 1), by
 // the element sum over the 24 tets of its star, evaluated at compile time:
@@ -218,6 +224,11 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 struct StreamArgs {
   double* out;          // y (APPLY), r (RESID), u_out (VEL, 3 fields), T (P1), p (P2)
@@ -602,138 +613,185 @@ __device__ __forceinline__ void finish_row(const DGrid& g, const StreamArgs& a, 
 
 template <int FORM, int OP>
 __global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP == OP_VEL) ? 2 : 3)
-    k_stream(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapP, DGrid g,
+    k_stream(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapP,
+             DGrid g,
              StreamArgs a) {
   constexpr int NF = OP == OP_P2 ? 1 : 4;
-  constexpr int SLOT = NF * FST;
-  constexpr uint32_t TX_BYTES = NF * PLANE * sizeof(double);  // bytes landed per plane
+  constexpr int NA = n_aux(OP);
+  constexpr int SLOT = slot_doubles(OP);
+  constexpr uint32_t TX_BYTES = NF * PLANE * sizeof(double);
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* smem_raw =
       smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);  // 1 KB aligned TMA destinations
   double* ring = reinterpret_cast<double*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + RING * SLOT * sizeof(double));
+  double* auxb = reinterpret_cast<double*>(bars + RING);  // [2][NA][NT] per-thread aux double buffer
 
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int ntx = g.n / TX;
   const int tiles = ntx * (g.n / TY);
-  const int sb = blockIdx.x;
-  const int tile = sb % tiles, chunk = sb / tiles;   // chunk-major: neighbours share L2
-  const int i0 = (tile % ntx) * TX, j0 = (tile / ntx) * TY;
-  const int kb = g.z0 + chunk * a.kchunk;
-  const int ke = min(kb + a.kchunk, g.z0 + g.nzl);
-  if (kb >= ke) return;
-  const int M = ke - kb + 2;  // planes kb-1 .. ke
-  const int kb1 = kb - 1;
-  const bool last_x = i0 + TX == g.n, last_y = j0 + TY == g.n;
-  const int i = i0 + tx, j = j0 + ty;
-  const int base = (ty + 1) * HX + (tx + 1);
-  // extra face rows: (n, j) for the last lane of last-x tiles, (i, n) for the
-  // last warp of last-y tiles, (n, n) for the last thread of the corner tile
-  const bool ex_x = last_x && tx == TX - 1, ex_y = last_y && ty == TY - 1, ex_c = ex_x && ex_y;
-  const bool any_ex = last_x || last_y;
+  const int nchunks = (g.nzl + a.kchunk - 1) / a.kchunk;
+  const int nitems = tiles * nchunks;  // (tile, z-chunk), chunk-major: neighbours share L2
+  const int G = gridDim.x;
+  // geometry of item `it`: tile origin, output planes [kb, ke), planes kb-1..ke staged
+  auto item_geom = [&](int it, int& ti0, int& tj0, int& tkb, int& tM) {
+    const int tile = it % tiles, chunk = it / tiles;
+    ti0 = (tile % ntx) * TX;
+    tj0 = (tile / ntx) * TY;
+    tkb = g.z0 + chunk * a.kchunk;
+    tM = min(tkb + a.kchunk, g.z0 + g.nzl) - tkb + 2;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RING; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto issue = [&](int m) {
-    if (m >= M) return;
-    const int s = m % RING;
-    const int P = kb1 + m;
+  // Producer (thread 0): the planes of this CTA's items, items blockIdx.x + q G,
+  // back to back; global plane sequence number S selects slot S % RING.
+  int pq = 0, pp = 0, pS = 0, pi0 = 0, pj0 = 0, pkb = 0, pM = 0;
+  bool pvalid = false;
+  if (threadIdx.x == 0 && (int)blockIdx.x < nitems) {
+    item_geom(blockIdx.x, pi0, pj0, pkb, pM);
+    pvalid = true;
+  }
+  auto issue_next = [&]() {  // thread 0: stage the next plane of the sequence
+    if (!pvalid) return;
+    const int s = pS % RING;
+    const int P = pkb - 1 + pp;
     fence_proxy_async();
     mbar_expect_tx(&bars[s], TX_BYTES);
     double* dst = ring + s * SLOT;
     if (NF == 4) {
       for (int f = 0; f < 3; ++f)
-        tma_load_4d(dst + f * FST, &mapU, &bars[s], i0 - 1 - a.ux0, j0 - 1 - a.uy0, P - a.uz0, f);
-      tma_load_4d(dst + 3 * FST, &mapP, &bars[s], i0, j0, P - g.z0 + 1, 0);
+        tma_load_4d(dst + f * FST, &mapU, &bars[s], pi0 - 1 - a.ux0, pj0 - 1 - a.uy0, P - a.uz0, f);
+      tma_load_4d(dst + 3 * FST, &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
     } else {
-      tma_load_4d(dst, &mapP, &bars[s], i0, j0, P - g.z0 + 1, 0);
+      tma_load_4d(dst, &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
+    }
+    ++pS;
+    if (++pp == pM) {
+      pp = 0;
+      ++pq;
+      const int it = blockIdx.x + pq * G;
+      pvalid = it < nitems;
+      if (pvalid) item_geom(it, pi0, pj0, pkb, pM);
     }
   };
   if (threadIdx.x == 0)
-    for (int m = 0; m < RING; ++m) issue(m);  // every slot is free at the start
+    for (int q = 0; q < RING - 2; ++q) issue_next();  // consumer iteration S stages plane S+RING-2
 
-  // iteration m (plane P = kb-1+m) uses accumulators (acc0, acc1, acc2) for
-  // outputs (P-1, P, P+1); R[] rotates by one per iteration (unrolled by 3)
-  Acc R0, R1, R2;
-  // m = 0 (plane kb-1): only output kb (its z-1 plane)
-  R2.zero();
-  mbar_wait(&bars[0], 0);
-  accumulate<FORM, OP, -1>(R2, ring, base);
-  // m = 1 (plane kb): outputs kb (in-plane) and kb+1 (z-1 plane)
-  R0.zero();
-  mbar_wait(&bars[1], 0);
-  accumulate<FORM, OP, 0>(R2, ring + SLOT, base);
-  accumulate<FORM, OP, -1>(R0, ring + SLOT, base);
-  int64_t o = vidx(g, i, j, kb);  // output row of the current iteration
-
-  auto body = [&](int m, Acc& acc0, Acc& acc1, Acc& acc2) {
-    const int k = kb1 + m - 1;  // output finished in this iteration
-    acc2.zero();
-    // early loads of per-output data (codes, own auxiliary values); consumed
-    // only after the accumulation, so their latency hides behind it
-    const uint8_t code = __ldg(g.code + o);
-    uint8_t cxy[3] = {0xFF, 0xFF, 0xFF};
-    if (any_ex) {
-      if (ex_x) cxy[0] = __ldg(g.code + o + 1);
-      if (ex_y) cxy[1] = __ldg(g.code + o + g.px);
-      if (ex_c) cxy[2] = __ldg(g.code + o + g.px + 1);
-    }
-    double aux[4] = {0, 0, 0, 0};
-    if (OP == OP_RESID) {
-#pragma unroll
-      for (int f = 0; f < 4; ++f) aux[f] = __ldg(a.aux + f * g.fs + o);
-    } else if (OP == OP_VEL) {
-#pragma unroll
-      for (int f = 0; f < 3; ++f) aux[f] = __ldg(a.aux + f * g.fs + o);
-    } else if (OP == OP_P1) {
-      aux[3] = __ldg(a.aux + o);
-    } else if (OP == OP_P2) {
-      aux[3] = a.out[o];
-    }
-    const int s = m % RING;
-    mbar_wait(&bars[s], (m / RING) & 1);
-    const double* pl = ring + s * SLOT;
-    accumulate<FORM, OP, 1>(acc0, pl, base);  // plane P is output P-1's z+1 plane
-    if (m < M - 1) {
-      accumulate<FORM, OP, 0>(acc1, pl, base);
-      accumulate<FORM, OP, -1>(acc2, pl, base);
-    }
-    const double* pls[3] = {ring + ((m + RING - 2) % RING) * SLOT, ring + ((m + RING - 1) % RING) * SLOT, pl};
-    if (!(code & (0x80 | CODE_TOP))) {
-      finish_row<FORM, OP>(g, a, i, j, k, o, code, aux, acc0, pls, base);
-    } else if (code != CODE_IRREGULAR) {
-      finish_top<FORM, OP>(g, a, i, j, k, o, code, aux, pls, base);
-    }
-    // face rows i = n, j = n (Dirichlet with an isoviscous star, else list rows)
-    if (any_ex) {
-      if (ex_x && !(cxy[0] & 0x80)) {
-        const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, false>(pls, base + 1);
-        finish_boundary<OP>(g, a, g.n, j, k, cxy[0], Bu, pls, base + 1);
-      }
-      if (ex_y && !(cxy[1] & 0x80)) {
-        const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<false, true>(pls, base + HX);
-        finish_boundary<OP>(g, a, i, g.n, k, cxy[1], Bu, pls, base + HX);
-      }
-      if (ex_c && !(cxy[2] & 0x80)) {
-        const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, true>(pls, base + HX + 1);
-        finish_boundary<OP>(g, a, g.n, g.n, k, cxy[2], Bu, pls, base + HX + 1);
-      }
-    }
-    __syncthreads();  // slot of plane m-2 is free for plane m+RING-2
-    if (threadIdx.x == 0) issue(m + RING - 2);
-    o += g.py;
+  int S = 0;  // consumer: global plane sequence number
+  auto wait_plane = [&]() -> const double* {
+    const int s = S % RING;
+    mbar_wait(&bars[s], (S / RING) & 1);
+    return ring + s * SLOT;
   };
-  int m = 2;
-  for (; m + 2 < M; m += 3) {
-    body(m, R2, R0, R1);
-    body(m + 1, R0, R1, R2);
-    body(m + 2, R1, R2, R0);
+  auto release = [&]() {  // all reads of plane S-2 are done: stage a new plane into its slot
+    __syncthreads();
+    if (threadIdx.x == 0) issue_next();
+    ++S;
+  };
+  const int i_ofs = tx, j_ofs = ty;
+  const int base = (ty + 1) * HX + (tx + 1);
+
+  for (int it = blockIdx.x; it < nitems; it += G) {
+    int i0, j0, kb, M;
+    item_geom(it, i0, j0, kb, M);
+    const int kb1 = kb - 1;
+    const bool last_x = i0 + TX == g.n, last_y = j0 + TY == g.n;
+    const int i = i0 + i_ofs, j = j0 + j_ofs;
+    // extra face rows: (n, j) for the last lane of last-x tiles, (i, n) for the
+    // last warp of last-y tiles, (n, n) for the last thread of the corner tile
+    const bool ex_x = last_x && tx == TX - 1, ex_y = last_y && ty == TY - 1, ex_c = ex_x && ex_y;
+    const bool any_ex = last_x || last_y;
+
+    // iteration m (plane P = kb-1+m) uses accumulators (acc0, acc1, acc2) for
+    // outputs (P-1, P, P+1); R[] rotates by one per iteration (unrolled by 3)
+    Acc R0, R1, R2;
+    // m = 0 (plane kb-1): only output kb (its z-1 plane)
+    R2.zero();
+    accumulate<FORM, OP, -1>(R2, wait_plane(), base);
+    release();
+    // m = 1 (plane kb): outputs kb (in-plane) and kb+1 (z-1 plane)
+    R0.zero();
+    {
+      const double* pl = wait_plane();
+      accumulate<FORM, OP, 0>(R2, pl, base);
+      accumulate<FORM, OP, -1>(R0, pl, base);
+    }
+    release();
+    int64_t o = vidx(g, i, j, kb);  // output row of the current iteration
+    uint8_t code_nx = __ldg(g.code + o);
+    // aux of row kb into buffer ab (cp.async group); each body prefetches the next row
+    const double* auxsrc = OP == OP_P2 ? a.out : a.aux;
+    auto aux_issue = [&](int64_t orow, int buf) {
+#pragma unroll
+      for (int f = 0; f < NA; ++f) cp_async8(auxb + (buf * NA + f) * NT + threadIdx.x, auxsrc + f * g.fs + orow);
+      cp_async_commit();
+    };
+    int ab = 0;
+    if (NA > 0) aux_issue(o, ab);
+
+    auto body = [&](int m, Acc& acc0, Acc& acc1, Acc& acc2) {
+      const int k = kb1 + m - 1;  // output finished in this iteration
+      acc2.zero();
+      // per-output data of row k, staged with plane k (previous slot, landed)
+      const uint8_t code = code_nx;           // loaded one iteration ahead
+      code_nx = __ldg(g.code + o + g.py);     // next row (the code array holds the halo planes)
+      uint8_t cxy[3] = {0xFF, 0xFF, 0xFF};
+      if (any_ex) {
+        if (ex_x) cxy[0] = __ldg(g.code + o + 1);
+        if (ex_y) cxy[1] = __ldg(g.code + o + g.px);
+        if (ex_c) cxy[2] = __ldg(g.code + o + g.px + 1);
+      }
+      double aux[4] = {0, 0, 0, 0};
+      if (NA > 0) {
+        aux_issue(o + g.py, ab ^ 1);  // next row (the slab holds the halo planes)
+        cp_async_wait1();             // this row's group has landed
+#pragma unroll
+        for (int f = 0; f < NA; ++f) aux[OP == OP_RESID || OP == OP_VEL ? f : 3] = auxb[(ab * NA + f) * NT + threadIdx.x];
+        ab ^= 1;
+      }
+      const double* pl = wait_plane();
+      accumulate<FORM, OP, 1>(acc0, pl, base);  // plane P is output P-1's z+1 plane
+      if (m < M - 1) {
+        accumulate<FORM, OP, 0>(acc1, pl, base);
+        accumulate<FORM, OP, -1>(acc2, pl, base);
+      }
+      const double* pls[3] = {ring + ((S + RING - 2) % RING) * SLOT, ring + ((S + RING - 1) % RING) * SLOT, pl};
+      if (!(code & (0x80 | CODE_TOP))) {
+        finish_row<FORM, OP>(g, a, i, j, k, o, code, aux, acc0, pls, base);
+      } else if (code != CODE_IRREGULAR) {
+        finish_top<FORM, OP>(g, a, i, j, k, o, code, aux, pls, base);
+      }
+      // face rows i = n, j = n (Dirichlet with an isoviscous star, else list rows)
+      if (any_ex) {
+        if (ex_x && !(cxy[0] & 0x80)) {
+          const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, false>(pls, base + 1);
+          finish_boundary<OP>(g, a, g.n, j, k, cxy[0], Bu, pls, base + 1);
+        }
+        if (ex_y && !(cxy[1] & 0x80)) {
+          const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<false, true>(pls, base + HX);
+          finish_boundary<OP>(g, a, i, g.n, k, cxy[1], Bu, pls, base + HX);
+        }
+        if (ex_c && !(cxy[2] & 0x80)) {
+          const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, true>(pls, base + HX + 1);
+          finish_boundary<OP>(g, a, g.n, g.n, k, cxy[2], Bu, pls, base + HX + 1);
+        }
+      }
+      release();
+      o += g.py;
+    };
+    int m = 2;
+    for (; m + 2 < M; m += 3) {
+      body(m, R2, R0, R1);
+      body(m + 1, R0, R1, R2);
+      body(m + 2, R1, R2, R0);
+    }
+    if (m < M) body(m, R2, R0, R1);
+    if (m + 1 < M) body(m + 1, R0, R1, R2);
   }
-  if (m < M) body(m, R2, R0, R1);
-  if (m + 1 < M) body(m + 1, R0, R1, R2);
 }
 
 // ---- host side --------------------------------------------------------------
@@ -810,8 +868,7 @@ inline bool assemble_stencils(cudaStream_t st) {
 }
 
 inline size_t stream_smem(int op) {
-  const int NF = op == OP_P2 ? 1 : 4;
-  return 1024 + RING * NF * FST * sizeof(double) + RING * sizeof(uint64_t);
+  return 1024 + RING * slot_doubles(op) * sizeof(double) + RING * sizeof(uint64_t) + 2 * n_aux(op) * NT * sizeof(double);
 }
 
 // the irregular-row list of a level (built by stk_assemble)
@@ -849,7 +906,7 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
     attr = true;
   }
   const int tiles = (g.n / TX) * (g.n / TY);
-  // z-chunks: about 4 waves of resident CTAs, 4..32 planes per chunk
+  // persistent grid: every resident CTA slot, items (tile, z-chunk) round robin
   static const int kchunk_env = getenv("STK_KCHUNK") ? atoi(getenv("STK_KCHUNK")) : 0;
   static int slots = 0;
   if (!slots) {
@@ -859,12 +916,14 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream<FORM, OP>, NT, sm);
     slots = std::max(1, nsm * std::max(1, per_sm));
   }
+  // chunk length: >= ~4 items per CTA for balance, 4..16 planes (short chunks keep
+  // concurrently streaming neighbour tiles at the same height: halos shared in L2)
   const int want = std::max(1, (4 * slots + tiles - 1) / tiles);
-  // (chunks of <= 32 planes keep concurrently streaming neighbour tiles at the
-  // same height, so their halo planes are shared through L2)
-  int kc = kchunk_env > 0 ? kchunk_env : std::min(32, std::max(4, (g.nzl + want - 1) / want));
+  int kc = kchunk_env > 0 ? kchunk_env : std::min(16, std::max(4, (g.nzl + want - 1) / want));
   kc = std::max(1, std::min(kc, g.nzl));
   const int chunks = (g.nzl + kc - 1) / kc;
+  const int nitems = tiles * chunks;
+  const int grid = std::min(nitems, slots);
   a.kchunk = kc;
   a.inU = inU;
   a.inP = inP;
@@ -878,7 +937,7 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
     if (cudaEventRecord(lv.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(lv.side, lv.ev_fork, 0) != cudaSuccess)
       return false;
   }
-  k_stream<FORM, OP><<<dim3(tiles * chunks), NT, sm, st>>>(mU, mP, g, a);
+  k_stream<FORM, OP><<<dim3(grid), NT, sm, st>>>(mU, mP, g, a);
   if (do_list) k_list<FORM, OP><<<(lv.n + LIST_NT - 1) / LIST_NT, LIST_NT, 0, fork ? lv.side : st>>>(g, a);
   if (fork) {
     if (cudaEventRecord(lv.ev_join, lv.side) != cudaSuccess || cudaStreamWaitEvent(st, lv.ev_join, 0) != cudaSuccess)
