@@ -189,6 +189,15 @@ stk_status stk_profile_enable(stk_ctx* ctx, int32_t on);
 stk_status stk_profile_reset(stk_ctx* ctx);
 stk_status stk_profile_read(stk_ctx* ctx, int32_t op, int32_t level, int64_t* launches, double* ms);
 
+/* Host only (no device needed): the z-slab partition of the level hierarchy that
+ * stk_create uses for (nranks, rank).  Writes *nlev and, per level l (finest
+ * first), out[8 l .. 8 l + 7] = {n_l, z0, nz_local, cz0, cz1, replicated, K0, K1}:
+ * owned vertex planes [z0, z0 + nz_local), stored cube layers [cz0, cz1), whether
+ * the level is held whole by every rank, and (for the last distributed level)
+ * the planes [K0, K1) of the next, replicated level this rank restricts into
+ * (-1 otherwise).  out must hold 8 * 16 int32.  STK_EINVAL on bad sizes. */
+stk_status stk_partition(int32_t n, int32_t n_coarse, int32_t nranks, int32_t rank, int32_t* nlev, int32_t* out);
+
 const char* stk_last_error(const stk_ctx* ctx);
 stk_status stk_destroy(stk_ctx* ctx);
 

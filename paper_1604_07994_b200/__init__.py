@@ -58,6 +58,7 @@ _P = ctypes.c_void_p
 _S = ctypes.c_int
 _sigs = {
     "stk_nccl_unique_id": [_P],
+    "stk_partition": [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P],
     "stk_create": [ctypes.POINTER(stk_config), _P, ctypes.POINTER(_P)],
     "stk_set_viscosity": [_P, _P, _P, ctypes.c_int32],
     "stk_cube_range": [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
@@ -111,6 +112,18 @@ def _ptr(t):
         return t.ctypes.data
     assert t.is_contiguous()
     return t.data_ptr()
+
+
+def partition(n, nranks, rank, n_coarse=4):
+    """z-slab partition of the level hierarchy (host only; stk_partition): list of
+    dicts per level (finest first) with n, z0, nzl, cz0, cz1, replicated, K0, K1."""
+    nlev = ctypes.c_int32()
+    out = (ctypes.c_int32 * (8 * 16))()
+    s = _lib.stk_partition(n, n_coarse, nranks, rank, ctypes.byref(nlev), out)
+    if s != STK_OK:
+        raise StkError("stk_partition", s, "bad sizes")
+    keys = ("n", "z0", "nzl", "cz0", "cz1", "replicated", "K0", "K1")
+    return [dict(zip(keys, out[8 * l:8 * l + 8])) for l in range(nlev.value)]
 
 
 def nccl_unique_id() -> bytes:

@@ -234,6 +234,34 @@ void host_tables(int8_t perm[6][3], int8_t corner[8][6], int8_t choff[6][8], int
   }
 }
 
+// ---- z-slab partition of the level hierarchy (host only) ------
+// Rank r of P owns vertex planes [r n_l/P, (r+1) n_l/P) of level l (the last rank
+// also k = n_l) and the cube layers its stars touch.  A level is distributed
+// while n_l/P >= 2 and it is not the coarsest; once a level is replicated every
+// coarser one is too (whole level on every rank, restriction gathers it).
+struct SlabLevel {
+  int n, z0, nzl, cz0, cz1, replicated, K0, K1;  // K0/K1: owned planes of the next (replicated) level, or -1
+};
+void slab_partition(int n, int nc, int P, int rank, std::vector<SlabLevel>& out) {
+  out.clear();
+  for (int m = n; m >= nc; m /= 2) out.push_back(SlabLevel{m, 0, 0, 0, 0, 0, -1, -1});
+  const int nlev = (int)out.size();
+  for (int l = 0; l < nlev; ++l) {
+    SlabLevel& L = out[l];
+    L.replicated = !(P == 1 || (L.n % P == 0 && L.n / P >= 2 && l < nlev - 1));
+    if (l > 0 && out[l - 1].replicated) L.replicated = 1;
+    const int r = L.replicated ? 0 : rank;
+    const int Pn = L.replicated ? 1 : P;
+    const int per = L.n / Pn;
+    L.z0 = r * per;
+    L.nzl = per + (r == Pn - 1 ? 1 : 0);
+    L.cz0 = std::max(0, L.z0 - 1);
+    L.cz1 = std::min(L.n, L.z0 + L.nzl);
+  }
+  for (int l = 0; l + 1 < nlev; ++l)
+    if (!out[l].replicated && out[l + 1].replicated) Comm::owned_coarse(out[l].n, P, rank, out[l].K0, out[l].K1);
+}
+
 // ---- level operations ------------------------------------------------------
 
 ListView lview(const stk_ctx* ctx, const Level& L) {
@@ -665,6 +693,22 @@ extern "C" {
 
 stk_status stk_nccl_unique_id(uint8_t id[128]) { return comm_unique_id(id); }
 
+stk_status stk_partition(int32_t n, int32_t n_coarse, int32_t nranks, int32_t rank, int32_t* nlev, int32_t* out) {
+  if (!nlev || !out || n < 4 || (n & (n - 1)) != 0 || nranks < 1 || rank < 0 || rank >= nranks) return STK_EINVAL;
+  const int nc = n_coarse > 0 ? n_coarse : 4;
+  if (nc > n || (nc & (nc - 1)) != 0) return STK_EINVAL;
+  std::vector<SlabLevel> part;
+  slab_partition(n, nc, nranks, rank, part);
+  if (part.size() > 16) return STK_EINVAL;
+  *nlev = (int32_t)part.size();
+  for (size_t l = 0; l < part.size(); ++l) {
+    const SlabLevel& L = part[l];
+    const int32_t v[8] = {L.n, L.z0, L.nzl, L.cz0, L.cz1, L.replicated, L.K0, L.K1};
+    memcpy(out + 8 * l, v, sizeof(v));
+  }
+  return STK_OK;
+}
+
 stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
   if (!cfg || !out) return STK_EINVAL;
   *out = nullptr;
@@ -709,24 +753,15 @@ stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
     ctx->lev.push_back(L);
   }
   ctx->nlev = (int)ctx->lev.size();
+  std::vector<SlabLevel> part;
+  slab_partition(n, nc, cfg->nranks, cfg->rank, part);
   for (int l = 0; l < ctx->nlev; ++l) {
     Level& L = ctx->lev[l];
-    const int P = cfg->nranks;
-    L.replicated = !(P == 1 || (L.n % P == 0 && L.n / P >= 2 && l < ctx->nlev - 1));
-    if (l > 0 && ctx->lev[l - 1].replicated) L.replicated = true;
-    if (!L.replicated && P > 1) {
-      // distributed levels need their coarse partner planes on the same rank
-      if ((L.n / P) % 2 != 0 && l + 1 < ctx->nlev) {
-        // next level becomes replicated (handled by its own flag)
-      }
-    }
-    const int r = L.replicated ? 0 : cfg->rank;
-    const int Pn = L.replicated ? 1 : P;
-    const int per = L.n / Pn;
-    L.z0 = r * per;
-    L.nzl = per + (r == Pn - 1 ? 1 : 0);
-    L.cz0 = std::max(0, L.z0 - 1);
-    L.cz1 = std::min(L.n, L.z0 + L.nzl);
+    L.replicated = part[l].replicated;
+    L.z0 = part[l].z0;
+    L.nzl = part[l].nzl;
+    L.cz0 = part[l].cz0;
+    L.cz1 = part[l].cz1;
     L.px = ((L.n + 3 + 15) / 16) * 16;  // ghost column i = -1, vertices 0..n, spare
     L.py = L.px * (L.n + 2);             // ghost row j = -1, rows 0..n
     L.fs = (((int64_t)(L.nzl + 2) * L.py + 31) / 32) * 32;
