@@ -174,6 +174,22 @@ stk_status stk_norms(stk_ctx* ctx, int32_t level, const double* x, double* out);
 /* Optional: select the kernel implementation for levels >= 64 intervals:
  * 1 = tiled constant-stencil kernels (default), 0 = generic element-row kernels. */
 stk_status stk_set_kernel_mode(stk_ctx* ctx, int32_t mode);
+/* Optional: inside the V-cycle, levels >= 1 with n_l <= row_n (default 16) run
+ * the lean one-thread-per-row kernels: constant stencils on isoviscous rows,
+ * explicit 4x4-block stencils (assembled by stk_assemble) on the
+ * Gamma_12 / Gamma_F rows.  0 = off (tiled / generic kernels).  Applies to the
+ * V-cycle only: stk_apply / stk_residual / stk_smooth keep their kernels.
+ * STK_EINVAL for row_n < 0. */
+stk_status stk_set_row_n(stk_ctx* ctx, int32_t row_n);
+/* First row-kernel level, or -1. */
+int32_t stk_row_level(const stk_ctx* ctx);
+/* Optional: row levels with n_l <= fuse_n that this rank holds whole run their
+ * part of the V-cycle as ONE persistent cooperative kernel with software grid
+ * barriers between the phases (default 0 = off: one launch per phase, replayed
+ * as a CUDA graph).  STK_EINVAL for fuse_n < 0. */
+stk_status stk_set_fuse_n(stk_ctx* ctx, int32_t fuse_n);
+/* First fused level, or -1 when the fused V-cycle is not used. */
+int32_t stk_fused_level(const stk_ctx* ctx);
 /* Number of kernels this context launched so far (evidence counter). */
 int64_t stk_launch_count(const stk_ctx* ctx);
 
@@ -183,7 +199,8 @@ int64_t stk_launch_count(const stk_ctx* ctx);
  * every launch is timed; on = 0: off.  stk_profile_read sums the records of
  * one op (0 apply, 1 residual, 2 velocity colour pass, 3 pressure pass 1,
  * 4 pressure pass 2, 5 restriction, 6 prolongation, 7 coarse solve,
- * 8 reductions, 9 Krylov vector ops, 10 coarse-level graph) on one level
+ * 8 reductions, 9 Krylov vector ops, 10 coarse-level graph, 11 fused
+ * coarse V-cycle kernel) on one level
  * (-1 = all); synchronises.  STK_EINVAL for on outside 0..2. */
 stk_status stk_profile_enable(stk_ctx* ctx, int32_t on);
 stk_status stk_profile_reset(stk_ctx* ctx);

@@ -77,6 +77,8 @@ _sigs = {
     "stk_gauge": [_P, ctypes.c_int32, _P],
     "stk_norms": [_P, ctypes.c_int32, _P, _P],
     "stk_set_kernel_mode": [_P, ctypes.c_int32],
+    "stk_set_fuse_n": [_P, ctypes.c_int32],
+    "stk_set_row_n": [_P, ctypes.c_int32],
     "stk_profile_enable": [_P, ctypes.c_int32],
     "stk_profile_reset": [_P],
     "stk_profile_read": [_P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
@@ -91,9 +93,13 @@ _lib.stk_last_error.argtypes = [_P]
 _lib.stk_last_error.restype = ctypes.c_char_p
 _lib.stk_launch_count.argtypes = [_P]
 _lib.stk_launch_count.restype = ctypes.c_int64
+_lib.stk_fused_level.argtypes = [_P]
+_lib.stk_fused_level.restype = ctypes.c_int32
+_lib.stk_row_level.argtypes = [_P]
+_lib.stk_row_level.restype = ctypes.c_int32
 
 # C names re-exported verbatim
-for _name in list(_sigs) + ["stk_last_error", "stk_launch_count"]:
+for _name in list(_sigs) + ["stk_last_error", "stk_launch_count", "stk_fused_level", "stk_row_level"]:
     globals()[_name] = getattr(_lib, _name)
 
 
@@ -216,11 +222,25 @@ class StokesContext:
     def set_kernel_mode(self, mode: int):
         self._chk("stk_set_kernel_mode", _lib.stk_set_kernel_mode(self.h, mode))
 
+    def set_fuse_n(self, fuse_n: int):
+        """Levels with n_l <= fuse_n run the V-cycle in one persistent kernel (0: off)."""
+        self._chk("stk_set_fuse_n", _lib.stk_set_fuse_n(self.h, fuse_n))
+
+    def set_row_n(self, row_n: int):
+        """V-cycle levels >= 1 with n_l <= row_n run the one-thread-per-row kernels (0: off)."""
+        self._chk("stk_set_row_n", _lib.stk_set_row_n(self.h, row_n))
+
+    def row_level(self) -> int:
+        return _lib.stk_row_level(self.h)
+
+    def fused_level(self) -> int:
+        return _lib.stk_fused_level(self.h)
+
     def launch_count(self) -> int:
         return _lib.stk_launch_count(self.h)
 
     PROFILE_OPS = ("apply", "residual", "vel_pass", "p_pass1", "p_pass2", "restrict", "prolong",
-                   "coarse", "reduce", "krylov", "coarse_graph")
+                   "coarse", "reduce", "krylov", "coarse_graph", "fused")
 
     def profile(self, on=True):
         """Event-time every launch: True/1 (the coarse-level CUDA graph timed as one

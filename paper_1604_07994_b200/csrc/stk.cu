@@ -14,6 +14,7 @@
 #include "comm.cuh"
 #include "kernels_generic.cuh"
 #include "kernels_tiled.cuh"
+#include "kernels_fused.cuh"
 #include "krylov.cuh"
 
 using namespace stk;
@@ -34,10 +35,15 @@ struct Level {
   int64_t nirr = 0;
   int32_t* list = nullptr;  // owned list rows (CODE_IRREGULAR), tiled levels only
   bool replicated = false;  // whole level held by every rank (coarse agglomeration)
+  // fused coarse levels (kernels_fused.cuh): explicit stencils of the non-regular rows
+  int32_t* slot = nullptr;  // owned linear index -> explicit slot or -1
+  int32_t* xrows = nullptr; // explicit rows (owned linear indices)
+  double* S = nullptr;      // explicit stencils [slot][EXPL]
+  int64_t nexpl = 0;
 };
 
 // event-timed profile of the kernels launched while enabled (stk_profile_*)
-enum { P_APPLY = 0, P_RESID, P_VEL, P_P1, P_P2, P_RESTRICT, P_PROLONG, P_COARSE, P_REDUCE, P_KRYLOV, P_CGRAPH, P_NOPS };
+enum { P_APPLY = 0, P_RESID, P_VEL, P_P1, P_P2, P_RESTRICT, P_PROLONG, P_COARSE, P_REDUCE, P_KRYLOV, P_CGRAPH, P_FUSED, P_NOPS };
 struct ProfRec {
   int op, level;
   cudaEvent_t e0, e1;
@@ -93,6 +99,16 @@ struct stk_ctx {
   cudaStream_t cap = nullptr;             // capture stream for the coarse-level CUDA graph
   cudaGraphExec_t coarse_exec = nullptr;  // levels >= 1 of the V-cycle (fixed internal buffers)
   int64_t coarse_launches = 0;            // kernels in that graph (launch accounting)
+  // fused coarse V-cycle (levels fl..nlev-1 in one persistent kernel), fl = -1: off
+  int fuse_n = 0;   // 0: fused persistent kernel off (one launch per phase in the graph)
+  int fl = -1;
+  int row_n = 16;   // levels >= 1 with n_l <= row_n run the row kernels (measured best, cfg2)
+  int rl = -1;      // first row level, -1: none
+  int fgrid = 0;
+  unsigned long long* fbar = nullptr;     // grid-barrier counters (one per prefix size)
+  FPhase* fprog = nullptr;                // phase program of the fused V-cycle (device)
+  int fnph = 0, fgrid_used = 0;
+  double* cfac = nullptr;                 // Gauss-Jordan column factors
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // reductions
   double* part = nullptr;
@@ -456,6 +472,174 @@ stk_status op_gauge(stk_ctx* ctx, int l, double* x) {
 
 stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x);
 
+// ---- row kernels of the context-owned coarse levels (kernels_fused.cuh) ---------
+bool row_level(const stk_ctx* ctx, int l) { return l >= 1 && l >= ctx->rl && ctx->rl > 0; }
+FLevel flevel(const stk_ctx* ctx, int l) {
+  const Level& L = ctx->lev[l];
+  FLevel F{};
+  F.g = dgrid(ctx, L);
+  F.x = L.x;
+  F.b = L.b;
+  F.r = L.r;
+  F.slot = L.slot;
+  F.S = L.S;
+  return F;
+}
+template <int OP, int LPR>
+void launch_rowl(stk_ctx* ctx, const FLevel& F, const FLevel& F2, int64_t rows, const double* uin, double* uout,
+                 int color) {
+  const unsigned nb = (unsigned)((rows * LPR + ROW_NT - 1) / ROW_NT);
+  const int nc = ctx->cfg.ncolors_u;
+  const double om = ctx->cfg.omega;
+  switch (ctx->cfg.form) {
+    case FORM_MOD: k_rowl<FORM_MOD, OP, LPR><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om); break;
+    case FORM_SYM: k_rowl<FORM_SYM, OP, LPR><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om); break;
+    default: k_rowl<FORM_GRAD, OP, LPR><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om); break;
+  }
+}
+// lanes per row: 16 (one Kuhn offset per lane) on the latency-bound small levels,
+// 4 on larger ones (fewer shuffles per row); STK_ROW_LPR overrides
+template <int OP>
+stk_status launch_row(stk_ctx* ctx, const FLevel& F, const FLevel& F2, int64_t rows, const double* uin = nullptr,
+                      double* uout = nullptr, int color = 0) {
+  static const int env = getenv("STK_ROW_LPR") ? atoi(getenv("STK_ROW_LPR")) : 0;
+  const int lpr = env == 1 || env == 4 || env == 16 ? env : (rows <= 40000 ? 16 : 4);
+  if (lpr == 16) launch_rowl<OP, 16>(ctx, F, F2, rows, uin, uout, color);
+  else if (lpr == 4) launch_rowl<OP, 4>(ctx, F, F2, rows, uin, uout, color);
+  else {
+    const unsigned nb = (unsigned)((rows + ROW_NT - 1) / ROW_NT);
+    const int nc = ctx->cfg.ncolors_u;
+    const double om = ctx->cfg.omega;
+    switch (ctx->cfg.form) {
+      case FORM_MOD: k_row<FORM_MOD, OP><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om); break;
+      case FORM_SYM: k_row<FORM_SYM, OP><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om); break;
+      default: k_row<FORM_GRAD, OP><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om); break;
+    }
+  }
+  return launched(ctx);
+}
+// one Uzawa step on a row level, in place on L.x with rhs L.b (as op_uzawa)
+stk_status op_uzawa_rows(stk_ctx* ctx, int l) {
+  Level& L = ctx->lev[l];
+  const FLevel F = flevel(ctx, l);
+  const int64_t V = owned_vertices(L);
+  const int nc = ctx->cfg.ncolors_u;
+  double* x = L.x;
+  double* tmp = L.r;
+  ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, x, 3, 1, L.replicated));
+  for (int s = 0; s < 2 * nc; ++s) {
+    const int color = s < nc ? s : 2 * nc - 1 - s;
+    const double* uin = (s & 1) ? tmp : x;
+    double* uout = (s & 1) ? x : tmp;
+    ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, const_cast<double*>(uin), 0, 3, L.replicated));
+    PScope ps(ctx, P_VEL, l);
+    ST(launch_row<FPH_VEL>(ctx, F, F, V, uin, uout, color));
+  }
+  ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, x, 0, 3, L.replicated));
+  {
+    PScope ps(ctx, P_P1, l);
+    ST(launch_row<FPH_P1>(ctx, F, F, V));
+  }
+  ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, tmp, 3, 1, L.replicated));
+  PScope ps(ctx, P_P2, l);
+  return launch_row<FPH_P2>(ctx, F, F, V);
+}
+stk_status op_residual_rows(stk_ctx* ctx, int l) {
+  Level& L = ctx->lev[l];
+  ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, L.x, 0, 4, L.replicated));
+  PScope ps(ctx, P_RESID, l);
+  return launch_row<FPH_RES>(ctx, flevel(ctx, l), flevel(ctx, l), owned_vertices(L));
+}
+// b_c = R r_f and x_c = 0 (both levels row levels, no agglomeration step between)
+stk_status op_restrict_rows(stk_ctx* ctx, int lf) {
+  Level& F = ctx->lev[lf];
+  ST(ctx->comm.halo(ctx, F.n, F.z0, F.nzl, F.py, F.fs, F.r, 0, 4, F.replicated));
+  PScope ps(ctx, P_RESTRICT, lf);
+  return launch_row<FPH_RESTRICT>(ctx, flevel(ctx, lf), flevel(ctx, lf + 1), owned_vertices(ctx->lev[lf + 1]));
+}
+stk_status op_prolong_rows(stk_ctx* ctx, int lc) {
+  Level& C = ctx->lev[lc];
+  ST(ctx->comm.halo(ctx, C.n, C.z0, C.nzl, C.py, C.fs, C.x, 0, 4, C.replicated));
+  PScope ps(ctx, P_PROLONG, lc);
+  return launch_row<FPH_PROLONG>(ctx, flevel(ctx, lc - 1), flevel(ctx, lc), owned_vertices(ctx->lev[lc - 1]));
+}
+stk_status op_coarse_rows(stk_ctx* ctx) {
+  PScope ps(ctx, P_COARSE, ctx->nlev - 1);
+  k_coarse_warp<<<(ctx->cN + 7) / 8, 256, 0, ctx->stream>>>(flevel(ctx, ctx->nlev - 1), ctx->cdofs, ctx->cG, ctx->cN,
+                                                           ctx->cN1);
+  return launched(ctx);
+}
+
+// V-cycle of the fused levels fl..nlev-1 on lev[fl].b (x from 0) in one persistent
+// cooperative kernel (kernels_fused.cuh)
+template <int FORM>
+stk_status launch_fused_t(stk_ctx* ctx) {
+  FusedArgs A{};
+  A.nl = ctx->nlev - ctx->fl;
+  for (int q = 0; q < A.nl; ++q) {
+    Level& L = ctx->lev[ctx->fl + q];
+    FLevel& F = A.L[q];
+    F.g = dgrid(ctx, L);
+    F.x = L.x;
+    F.b = L.b;
+    F.r = L.r;
+    F.slot = L.slot;
+    F.S = L.S;
+  }
+  A.nph = ctx->fnph;
+  A.prog = ctx->fprog;
+  A.ncolors = ctx->cfg.ncolors_u;
+  A.omega = ctx->cfg.omega;
+  A.cdofs = ctx->cdofs;
+  A.cG = ctx->cG;
+  A.cN = ctx->cN;
+  A.cld = ctx->cN1;
+  A.bar = ctx->fbar;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(ctx->fgrid_used);
+  lc.blockDim = dim3(256);
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  static const bool trace = getenv("STK_FUSED_TRACE") && atoi(getenv("STK_FUSED_TRACE"));
+  static unsigned long long* tbuf = nullptr;
+  if (trace && !tbuf) CK(cudaMallocManaged(&tbuf, sizeof(unsigned long long) * (FPH_MAX + 1)));
+  A.trace = trace ? tbuf : nullptr;
+  CK(cudaLaunchKernelEx(&lc, k_mg_fused<FORM>, A));
+  if (trace) {  // debug: per-phase durations (CTA 0 clock after each phase's barrier)
+    CK(cudaStreamSynchronize(ctx->stream));
+    static const char* nm[] = {"zero", "vel", "p1", "p2", "resid", "restrict", "prolong", "coarse"};
+    std::vector<FPhase> hp(ctx->fnph);
+    CK(cudaMemcpy(hp.data(), ctx->fprog, sizeof(FPhase) * ctx->fnph, cudaMemcpyDeviceToHost));
+    std::vector<std::pair<std::string, std::pair<double, int>>> agg;
+    unsigned long long prev = tbuf[FPH_MAX];
+    for (int k = 0; k < ctx->fnph; ++k) {
+      const double dt = (tbuf[k] - prev) * 1e-3;
+      prev = tbuf[k];
+      const std::string key = "L" + std::to_string(hp[k].lev) + " " + nm[hp[k].op] + " m=" + std::to_string(hp[k].m);
+      bool found = false;
+      for (auto& e : agg)
+        if (e.first == key) { e.second.first += dt; e.second.second++; found = true; }
+      if (!found) agg.push_back({key, {dt, 1}});
+    }
+    for (auto& e : agg)
+      fprintf(stderr, "  %-24s %4d x %8.2f us = %9.1f us\n", e.first.c_str(), e.second.second,
+              e.second.first / e.second.second, e.second.first);
+  }
+  return launched(ctx);
+}
+stk_status op_fused(stk_ctx* ctx) {
+  PScope ps(ctx, P_FUSED, ctx->fl);
+  switch (ctx->cfg.form) {
+    case FORM_MOD: return launch_fused_t<FORM_MOD>(ctx);
+    case FORM_SYM: return launch_fused_t<FORM_SYM>(ctx);
+    default: return launch_fused_t<FORM_GRAD>(ctx);
+  }
+}
+
 // lev[1].x = V-cycle of levels >= 1 on lev[1].b from a zero guess.  These
 // levels only touch context-owned buffers, so the whole sequence (a few hundred
 // small launches with the V_var schedule) is captured once into a CUDA graph
@@ -463,6 +647,7 @@ stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x);
 stk_status op_coarse_part(stk_ctx* ctx) {
   Level& C = ctx->lev[1];
   static const bool no_graph = getenv("STK_NO_GRAPH") && atoi(getenv("STK_NO_GRAPH"));
+  if (ctx->fl == 1) return op_fused(ctx);  // one launch: nothing to capture
   if (ctx->prof.on == 2 || no_graph) {
     CK(cudaMemsetAsync(C.x, 0, sizeof(double) * C.vlen, ctx->stream));
     return op_vcycle(ctx, 1, C.b, C.x);
@@ -504,23 +689,29 @@ stk_status op_coarse_part(stk_ctx* ctx) {
   return STK_OK;
 }
 
+// V_var cycle (R13) on level l.  Levels >= 1 are context-owned
+// (b = lev[l].b, x = lev[l].x); row levels (n_l <= row_n) run the lean row kernels.
 stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x) {
-  if (l == ctx->nlev - 1) return op_coarse(ctx, b, x);
+  if (l == ctx->nlev - 1) return row_level(ctx, l) ? op_coarse_rows(ctx) : op_coarse(ctx, b, x);
   Level& L = ctx->lev[l];
   Level& C = ctx->lev[l + 1];
+  const bool rows = row_level(ctx, l);
   const int nu_pre = ctx->cfg.nu_pre + ctx->cfg.nu_inc * l;
   const int nu_post = ctx->cfg.nu_post + ctx->cfg.nu_inc * l;
-  for (int s = 0; s < nu_pre; ++s) ST(op_uzawa(ctx, l, x, b));
-  ST(op_residual(ctx, l, x, b, L.r));
-  ST(op_restrict(ctx, l, L.r, C.b));
+  for (int s = 0; s < nu_pre; ++s) ST(rows ? op_uzawa_rows(ctx, l) : op_uzawa(ctx, l, x, b));
+  ST(rows ? op_residual_rows(ctx, l) : op_residual(ctx, l, x, b, L.r));
+  const bool rows_tr = rows && row_level(ctx, l + 1) && (C.replicated == L.replicated);
+  ST(rows_tr ? op_restrict_rows(ctx, l) : op_restrict(ctx, l, L.r, C.b));
   if (l == 0) {
     ST(op_coarse_part(ctx));
+  } else if (l + 1 == ctx->fl) {
+    ST(op_fused(ctx));
   } else {
-    CK(cudaMemsetAsync(C.x, 0, sizeof(double) * C.vlen, ctx->stream));
+    if (!rows_tr) CK(cudaMemsetAsync(C.x, 0, sizeof(double) * C.vlen, ctx->stream));
     ST(op_vcycle(ctx, l + 1, C.b, C.x));
   }
-  ST(op_prolong_add(ctx, l + 1, C.x, x));
-  for (int s = 0; s < nu_post; ++s) ST(op_uzawa(ctx, l, x, b));
+  ST(rows_tr ? op_prolong_rows(ctx, l + 1) : op_prolong_add(ctx, l + 1, C.x, x));
+  for (int s = 0; s < nu_post; ++s) ST(rows ? op_uzawa_rows(ctx, l) : op_uzawa(ctx, l, x, b));
   return STK_OK;
 }
 
@@ -659,6 +850,137 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
     rel = bnorm > 0 ? beta / bnorm : 0.0;  // true residual after the restart
     if (its < 256) R->res_hist[its] = rel;
   }
+  return STK_OK;
+}
+
+// persistent-grid size (one 256-thread CTA per SM) and the barrier words
+stk_status fused_setup(stk_ctx* ctx) {
+  if (!ctx->fbar) {
+    int dev = 0, nsm = 0, per = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mg_fused<FORM_SYM>, 256, 0));
+    int per2 = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_gauss_jordan_coop, 256, 0));
+    per = std::min(per, per2);
+    ctx->fgrid = std::max(1, nsm * std::max(1, per));
+    const size_t words = (size_t)(ctx->fgrid + 2);
+    CK(cudaMalloc(&ctx->fbar, sizeof(unsigned long long) * words));
+    CK(cudaMemsetAsync(ctx->fbar, 0, sizeof(unsigned long long) * words, ctx->stream));
+  }
+  return STK_OK;
+}
+
+// first fused level: n_l <= fuse_n, below the finest, every level from there
+// on held whole by this rank; explicit stencils of its non-regular rows
+stk_status fused_assemble(stk_ctx* ctx) {
+  ctx->fl = -1;
+  for (auto& L : ctx->lev) {
+    cudaFree(L.slot);
+    cudaFree(L.xrows);
+    cudaFree(L.S);
+    L.slot = L.xrows = nullptr;
+    L.S = nullptr;
+    L.nexpl = 0;
+  }
+  ctx->rl = -1;
+  if (ctx->kernel_mode != 1) return STK_OK;
+  int rl = -1;
+  for (int l = 1; l < ctx->nlev; ++l)
+    if (ctx->lev[l].n <= ctx->row_n) {
+      rl = l;
+      break;
+    }
+  if (rl < 0) return STK_OK;
+  int fl = -1;
+  if (ctx->fuse_n > 0)
+    for (int l = ctx->nlev - 2; l >= rl; --l) {
+      const Level& L = ctx->lev[l];
+      if (L.n > ctx->fuse_n || (ctx->cfg.nranks > 1 && !L.replicated) || ctx->nlev - l > FMAX) break;
+      fl = l;
+    }
+  ST(assemble_stencils(ctx->stream) ? STK_OK : STK_ECUDA);
+  unsigned long long* dcnt;
+  CK(cudaMalloc(&dcnt, sizeof(unsigned long long)));
+  for (int l = rl; l < ctx->nlev; ++l) {
+    Level& L = ctx->lev[l];
+    const int64_t V = owned_vertices(L);
+    CK(cudaMalloc(&L.slot, sizeof(int32_t) * L.fs));
+    CK(cudaMalloc(&L.xrows, sizeof(int32_t) * V));
+    CK(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long), ctx->stream));
+    k_build_explicit<<<nblocks(V), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), L.slot, L.xrows, dcnt);
+    ST(launched(ctx));
+    unsigned long long c = 0;
+    CK(cudaMemcpyAsync(&c, dcnt, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    L.nexpl = (int64_t)c;
+    if (c == 0) continue;
+    CK(cudaMalloc(&L.S, sizeof(double) * EXPL * c));
+    const unsigned nb = nblocks((int64_t)c * NQ * 4);
+    DGrid g = dgrid(ctx, L);
+    switch (ctx->cfg.form) {
+      case FORM_MOD: k_assemble_explicit<FORM_MOD><<<nb, kThreads, 0, ctx->stream>>>(g, L.xrows, (int)c, L.S); break;
+      case FORM_SYM: k_assemble_explicit<FORM_SYM><<<nb, kThreads, 0, ctx->stream>>>(g, L.xrows, (int)c, L.S); break;
+      default: k_assemble_explicit<FORM_GRAD><<<nb, kThreads, 0, ctx->stream>>>(g, L.xrows, (int)c, L.S); break;
+    }
+    ST(launched(ctx));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(dcnt);
+  ctx->rl = rl;
+  if (fl < 0) return STK_OK;
+  // phase program (the V-cycle of op_vcycle / op_uzawa restricted to levels fl..)
+  static const int single = getenv("STK_FUSED_SINGLE") ? atoi(getenv("STK_FUSED_SINGLE")) : 1000;
+  const int nl = ctx->nlev - fl;
+  std::vector<int> m(nl);
+  for (int q = 0; q < nl; ++q) {
+    const int64_t V = owned_vertices(ctx->lev[fl + q]);
+    m[q] = V <= single ? 1 : std::max(1, std::min(ctx->fgrid, (int)((V + 255) / 256)));
+  }
+  const int mc = m[nl - 1] == 1 ? 1 : std::max(1, std::min(ctx->fgrid, (ctx->cN + 7) / 8));
+  std::vector<FPhase> prog;
+  auto add = [&](int op, int lev, int mm, int color = 0, int flip = 0) {
+    FPhase P{};
+    P.op = (uint8_t)op;
+    P.lev = (uint8_t)lev;
+    P.color = (uint8_t)color;
+    P.flip = (uint8_t)flip;
+    P.m = (int16_t)mm;
+    prog.push_back(P);
+  };
+  const int nc = ctx->cfg.ncolors_u;
+  auto uzawa = [&](int q) {
+    for (int s = 0; s < 2 * nc; ++s) add(FPH_VEL, q, m[q], s < nc ? s : 2 * nc - 1 - s, s & 1);
+    add(FPH_P1, q, m[q]);
+    add(FPH_P2, q, m[q]);
+  };
+  add(FPH_ZERO, 0, m[0]);
+  for (int q = 0; q + 1 < nl; ++q) {
+    const int nu = ctx->cfg.nu_pre + ctx->cfg.nu_inc * (fl + q);
+    for (int s = 0; s < nu; ++s) uzawa(q);
+    add(FPH_RES, q, m[q]);
+    add(FPH_RESTRICT, q, m[q + 1]);
+  }
+  add(FPH_COARSE, nl - 1, mc);
+  for (int q = nl - 2; q >= 0; --q) {
+    const int nu = ctx->cfg.nu_post + ctx->cfg.nu_inc * (fl + q);
+    add(FPH_PROLONG, q, m[q]);
+    for (int s = 0; s < nu; ++s) uzawa(q);
+  }
+  if ((int)prog.size() > FPH_MAX) return STK_OK;  // too long: per-phase launches
+  int gmax = 1;
+  for (size_t k = 0; k < prog.size(); ++k) {
+    const int next = k + 1 < prog.size() ? prog[k + 1].m : 0;
+    prog[k].barM = (int16_t)(next ? std::max<int>(prog[k].m, next) : 0);
+    gmax = std::max<int>(gmax, prog[k].m);
+  }
+  cudaFree(ctx->fprog);
+  ctx->fprog = nullptr;
+  CK(cudaMalloc(&ctx->fprog, sizeof(FPhase) * prog.size()));
+  CK(cudaMemcpy(ctx->fprog, prog.data(), sizeof(FPhase) * prog.size(), cudaMemcpyHostToDevice));
+  ctx->fnph = (int)prog.size();
+  ctx->fgrid_used = gmax;
+  ctx->fl = fl;
   return STK_OK;
 }
 
@@ -925,8 +1247,24 @@ stk_status stk_assemble(stk_ctx* ctx) {
   }
   ST(launched(ctx));
   CK(cudaMemsetAsync(ctx->cstatus, 0, sizeof(int), ctx->stream));
-  k_gauss_jordan<<<1, 1024, 0, ctx->stream>>>(ctx->cK, ctx->cG, N1, ctx->cstatus);
-  ST(launched(ctx));
+  ST(fused_setup(ctx));  // grid size + barrier words (used by the coarse inverse too)
+  {
+    cudaFree(ctx->cfac);
+    ctx->cfac = nullptr;
+    CK(cudaMalloc(&ctx->cfac, sizeof(double) * N1));
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(std::min(ctx->fgrid, std::max(1, (N1 * N1 + 255) / 256)));
+    lc.blockDim = dim3(256);
+    lc.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, k_gauss_jordan_coop, ctx->cK, ctx->cG, ctx->cfac, N1, ctx->cstatus, ctx->fbar));
+    ST(launched(ctx));
+  }
+  ST(fused_assemble(ctx));
   int hs = 0;
   CK(cudaMemcpyAsync(&hs, ctx->cstatus, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1132,8 +1470,29 @@ stk_status stk_set_kernel_mode(stk_ctx* ctx, int32_t mode) {
   if (!ctx || (mode != 0 && mode != 1)) return STK_EINVAL;
   ctx->kernel_mode = mode;
   drop_graphs(ctx);
+  if (ctx->state >= 2) ST(fused_assemble(ctx));
   return STK_OK;
 }
+
+stk_status stk_set_fuse_n(stk_ctx* ctx, int32_t fuse_n) {
+  if (!ctx || fuse_n < 0) return STK_EINVAL;
+  ctx->fuse_n = fuse_n;
+  drop_graphs(ctx);
+  if (ctx->state >= 2) ST(fused_assemble(ctx));
+  return STK_OK;
+}
+
+int32_t stk_fused_level(const stk_ctx* ctx) { return ctx ? ctx->fl : -1; }
+
+stk_status stk_set_row_n(stk_ctx* ctx, int32_t row_n) {
+  if (!ctx || row_n < 0) return STK_EINVAL;
+  ctx->row_n = row_n;
+  drop_graphs(ctx);
+  if (ctx->state >= 2) ST(fused_assemble(ctx));
+  return STK_OK;
+}
+
+int32_t stk_row_level(const stk_ctx* ctx) { return ctx ? ctx->rl : -1; }
 
 int64_t stk_launch_count(const stk_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
@@ -1179,7 +1538,13 @@ stk_status stk_destroy(stk_ctx* ctx) {
     cudaFree(L.x);
     cudaFree(L.b);
     cudaFree(L.r);
+    cudaFree(L.slot);
+    cudaFree(L.xrows);
+    cudaFree(L.S);
   }
+  cudaFree(ctx->fbar);
+  cudaFree(ctx->fprog);
+  cudaFree(ctx->cfac);
   cudaFree(ctx->cdofs);
   cudaFree(ctx->cK);
   cudaFree(ctx->cG);

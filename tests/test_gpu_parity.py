@@ -274,3 +274,39 @@ def test_tiled_equals_generic_device_path():
     y0 = ctx.export(ctx.apply(xv))
     err, errs = per_field_rel(y1, y0)
     assert err <= 1e-13, errs
+
+
+@pytest.mark.parametrize("cfgname,n,form", [("cfg1", 16, "mod"), ("cfg2", 64, "mod"), ("cfg2", 32, "sym"),
+                                            ("cfg3", 64, "grad"), ("cfg5", 64, "mod")])
+def test_coarse_level_kernel_paths_agree(cfgname, n, form):
+    """The three device paths of the coarse V-cycle levels agree: the lean row
+    kernels (default; explicit stencils on the Gamma rows), the element-row /
+    tiled kernels (row_n = 0) and the fused persistent kernel (fuse_n = 32).
+    test_uzawa_step_and_vcycle pins the default path to the oracle multigrid."""
+    nc = 4 if form == "sym" else 2
+    ctx, cfg, cls, fcls = make_ctx(cfgname, n, form, kernel_mode=1, ncolors_u=nc)
+    ctx.set_row_n(32)
+    assert ctx.row_level() >= 1 and ctx.fused_level() == -1
+    rng = np.random.default_rng(11)
+    V = (n + 1) ** 3
+    x = rng.uniform(-1, 1, (4, V))
+    b = rng.uniform(-1, 1, (4, V)) * 1e-3
+    bg = ctx.import_(b)
+
+    def two_cycles():
+        xg = ctx.import_(x)
+        for _ in range(2):
+            ctx.vcycle(bg, xg)
+        return ctx.export(xg)
+
+    y_rows = two_cycles()
+    ctx.set_row_n(0)
+    assert ctx.row_level() == -1
+    y_generic = two_cycles()
+    ctx.set_row_n(32)
+    ctx.set_fuse_n(32)
+    assert ctx.fused_level() >= 1
+    y_fused = two_cycles()
+    for other in (y_generic, y_fused):
+        err, errs = per_field_rel(y_rows, other)
+        assert err <= 1e-12, errs
