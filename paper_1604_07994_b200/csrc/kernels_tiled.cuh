@@ -265,19 +265,18 @@ struct Acc {
 };
 
 // contribution of staged in-plane point Q (offset (kdx(Q), kdy(Q)) from the
-// output column, plane offset DZ from the output row) to one output row
+// output column, plane offset DZ from the output row) to one output row, from
+// the point's values already in registers (u0, u1, u2, p)
 template <int FORM, int OP, int DZ, int Q>
-__device__ __forceinline__ void acc_q(Acc& acc, const double* __restrict__ pl, int base) {
+__device__ __forceinline__ void acc_v(Acc& acc, double u0, double u1, double u2, double p) {
   constexpr int dx = kdx(Q), dy = kdy(Q);
   if constexpr (kuhn(dx, dy, DZ)) {
     constexpr bool NEED_U = OP != OP_P1 && OP != OP_P2;  // A, B^T rows
     constexpr bool NEED_P = OP != OP_VEL;                // B, C rows
     constexpr double kC = KS<3, 0, 0, 0, dx, dy, DZ>::v;
-    const int s = base + dy * HX + dx;
     if constexpr (OP == OP_P2) {
-      if constexpr (kC != 0.0) acc.C = fma(kC, pl[s], acc.C);
+      if constexpr (kC != 0.0) acc.C = fma(kC, p, acc.C);
     } else {
-      const double u0 = pl[s], u1 = pl[FST + s], u2 = pl[2 * FST + s], p = pl[3 * FST + s];
       if constexpr (NEED_U) {
         if constexpr (FORM == FORM_SYM) {
           acc.A[0] = fma(KS<0, FORM_SYM, 0, 0, dx, dy, DZ>::v, u0, acc.A[0]);
@@ -315,15 +314,45 @@ __device__ __forceinline__ void acc_q(Acc& acc, const double* __restrict__ pl, i
   }
 }
 
+// point Q of a landed plane: its values are read from shared memory ONCE and
+// added to the outputs one plane below (acc0, DZ = +1), in the plane (acc1, DZ = 0)
+// and one plane above (acc2, DZ = -1); MASK: bit0 acc0, bit1 acc1, bit2 acc2
+template <int FORM, int OP, int Q, int MASK>
+__device__ __forceinline__ void point3(Acc& acc0, Acc& acc1, Acc& acc2, const double* __restrict__ pl, int base) {
+  constexpr int dx = kdx(Q), dy = kdy(Q);
+  constexpr bool U0 = (MASK & 1) && kuhn(dx, dy, 1), U1 = (MASK & 2) && kuhn(dx, dy, 0), U2 = (MASK & 4) && kuhn(dx, dy, -1);
+  if constexpr (U0 || U1 || U2) {
+    const int s = base + dy * HX + dx;
+    double u0 = 0.0, u1 = 0.0, u2 = 0.0, p;
+    if constexpr (OP == OP_P2) {
+      p = pl[s];
+    } else {
+      u0 = pl[s];
+      u1 = pl[FST + s];
+      u2 = pl[2 * FST + s];
+      p = pl[3 * FST + s];
+    }
+    if constexpr (U0) acc_v<FORM, OP, 1, Q>(acc0, u0, u1, u2, p);
+    if constexpr (U1) acc_v<FORM, OP, 0, Q>(acc1, u0, u1, u2, p);
+    if constexpr (U2) acc_v<FORM, OP, -1, Q>(acc2, u0, u1, u2, p);
+  }
+}
+template <int FORM, int OP, int MASK>
+__device__ __forceinline__ void accumulate3(Acc& acc0, Acc& acc1, Acc& acc2, const double* __restrict__ pl, int base) {
+  point3<FORM, OP, 0, MASK>(acc0, acc1, acc2, pl, base);
+  point3<FORM, OP, 1, MASK>(acc0, acc1, acc2, pl, base);
+  point3<FORM, OP, 2, MASK>(acc0, acc1, acc2, pl, base);
+  point3<FORM, OP, 3, MASK>(acc0, acc1, acc2, pl, base);
+  point3<FORM, OP, 4, MASK>(acc0, acc1, acc2, pl, base);
+  point3<FORM, OP, 5, MASK>(acc0, acc1, acc2, pl, base);
+  point3<FORM, OP, 6, MASK>(acc0, acc1, acc2, pl, base);
+}
+// single-output form (prologue planes)
 template <int FORM, int OP, int DZ>
 __device__ __forceinline__ void accumulate(Acc& acc, const double* __restrict__ pl, int base) {
-  acc_q<FORM, OP, DZ, 0>(acc, pl, base);
-  acc_q<FORM, OP, DZ, 1>(acc, pl, base);
-  acc_q<FORM, OP, DZ, 2>(acc, pl, base);
-  acc_q<FORM, OP, DZ, 3>(acc, pl, base);
-  acc_q<FORM, OP, DZ, 4>(acc, pl, base);
-  acc_q<FORM, OP, DZ, 5>(acc, pl, base);
-  acc_q<FORM, OP, DZ, 6>(acc, pl, base);
+  if constexpr (DZ == 1) accumulate3<FORM, OP, 1>(acc, acc, acc, pl, base);
+  else if constexpr (DZ == 0) accumulate3<FORM, OP, 2>(acc, acc, acc, pl, base);
+  else accumulate3<FORM, OP, 4>(acc, acc, acc, pl, base);
 }
 
 // Truncated-star C row of an isoviscous boundary vertex in unit form:
@@ -430,7 +459,7 @@ __device__ __forceinline__ void list_row(const DGrid& g, const StreamArgs& a, in
       a.out[f * g.fs + o] = v;
     }
   } else if (OP == OP_VEL) {
-    const bool act = ((i + j + k) % a.ncolors) == a.color && !dir;
+    const bool act = ((i + j + k) & (a.ncolors - 1)) == a.color && !dir;
     if (act) row_list<FORM, false>(g, i, j, k, a.inU, a.inP, BLK_A | BLK_BT, y, dA, dC);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -539,20 +568,21 @@ __device__ __forceinline__ void finish_top(const DGrid& g, const StreamArgs& a, 
 #pragma unroll
     for (int f = 0; f < 4; ++f) a.out[f * g.fs + o] = OP == OP_RESID ? aux[f] - y[f] : y[f];
   } else if (OP == OP_VEL) {
-    const bool act = ((i + j + k) % a.ncolors) == a.color;
-    const double kd[3] = {kAd0, kAd1, kAd2};
+    const bool act = ((i + j + k) & (a.ncolors - 1)) == a.color;
+    const double isA = imu * (double)g.n * 6.0;
+    const double ikd[3] = {1.0 / kAd0, 1.0 / kAd1, 1.0 / kAd2};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double uc = pls[1][c * FST + base];
-      a.out[c * g.fs + o] = act ? uc + (aux[c] - fma(sA, acc.A[c], sB * acc.BT[c])) / (sA * kd[c]) : uc;
+      a.out[c * g.fs + o] = act ? fma(aux[c] - fma(sA, acc.A[c], sB * acc.BT[c]), isA * ikd[c], uc) : uc;
     }
   } else if (OP == OP_P1) {
     const double r = fma(sB, acc.B, -sC * acc.C) - aux[3];
-    a.out[o] = ((i + j + k) & 1) == 0 ? r / (sC * kCd) : r;
+    a.out[o] = ((i + j + k) & 1) == 0 ? r * (mu * (6.0 / kCd) * g.idh3) : r;
   } else {
     const double T = pls[1][base];
     double d = T;
-    if ((i + j + k) & 1) d = (T - sC * (acc.C - kCd * T)) / (sC * kCd);
+    if ((i + j + k) & 1) d = (T - sC * (acc.C - kCd * T)) * (mu * (6.0 / kCd) * g.idh3);
     a.out[o] = aux[3] + a.omega * d;
   }
 }
@@ -590,23 +620,25 @@ __device__ __forceinline__ void finish_row(const DGrid& g, const StreamArgs& a, 
 #pragma unroll
     for (int f = 0; f < 4; ++f) a.out[f * g.fs + o] = OP == OP_RESID ? aux[f] - y[f] : y[f];
   } else if (OP == OP_VEL) {
-    const bool act = ((i + j + k) % a.ncolors) == a.color;
+    const bool act = ((i + j + k) & (a.ncolors - 1)) == a.color;
     const double* cpl = pls[1];
-    const double kd[3] = {kAd0, kAd1, kAd2};
+    // 1 / (sA kd) = 6 n / (mu kd): the Gauss-Seidel diagonal without a division
+    const double isA = imu * (double)g.n * 6.0;
+    const double ikd[3] = {1.0 / kAd0, 1.0 / kAd1, 1.0 / kAd2};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double uc = cpl[c * FST + base];
       double v = uc;
-      if (act) v = uc + (aux[c] - fma(sA, acc.A[c], sB * acc.BT[c])) / (sA * kd[c]);
+      if (act) v = fma(aux[c] - fma(sA, acc.A[c], sB * acc.BT[c]), isA * ikd[c], uc);
       a.out[c * g.fs + o] = v;
     }
   } else if (OP == OP_P1) {
     const double r = fma(sB, acc.B, -sC * acc.C) - aux[3];
-    a.out[o] = ((i + j + k) & 1) == 0 ? r / (sC * kCd) : r;
+    a.out[o] = ((i + j + k) & 1) == 0 ? r * (mu * (6.0 / kCd) * g.idh3) : r;
   } else {  // P2: acc.C = sum_o 6C(o) T (incl. the centre); neighbours of colour 1 are colour 0
     const double T = pls[1][base];
     double d = T;
-    if ((i + j + k) & 1) d = (T - sC * (acc.C - kCd * T)) / (sC * kCd);
+    if ((i + j + k) & 1) d = (T - sC * (acc.C - kCd * T)) * (mu * (6.0 / kCd) * g.idh3);
     a.out[o] = aux[3] + a.omega * d;
   }
 }
@@ -717,8 +749,7 @@ __global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP ==
     R0.zero();
     {
       const double* pl = wait_plane();
-      accumulate<FORM, OP, 0>(R2, pl, base);
-      accumulate<FORM, OP, -1>(R0, pl, base);
+      accumulate3<FORM, OP, 6>(R0, R2, R0, pl, base);  // R2: in-plane (output kb), R0: output kb+1
     }
     release();
     int64_t o = vidx(g, i, j, kb);  // output row of the current iteration
@@ -754,11 +785,9 @@ __global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP ==
         ab ^= 1;
       }
       const double* pl = wait_plane();
-      accumulate<FORM, OP, 1>(acc0, pl, base);  // plane P is output P-1's z+1 plane
-      if (m < M - 1) {
-        accumulate<FORM, OP, 0>(acc1, pl, base);
-        accumulate<FORM, OP, -1>(acc2, pl, base);
-      }
+      // plane P is output P-1's z+1 plane, output P's own plane, output P+1's z-1 plane
+      if (m < M - 1) accumulate3<FORM, OP, 7>(acc0, acc1, acc2, pl, base);
+      else accumulate3<FORM, OP, 1>(acc0, acc1, acc2, pl, base);
       const double* pls[3] = {ring + ((S + RING - 2) % RING) * SLOT, ring + ((S + RING - 1) % RING) * SLOT, pl};
       if (!(code & (0x80 | CODE_TOP))) {
         finish_row<FORM, OP>(g, a, i, j, k, o, code, aux, acc0, pls, base);

@@ -193,6 +193,7 @@ DGrid dgrid(const stk_ctx* ctx, const Level& L) {
   g.fs = L.fs;
   g.h = L.h;
   g.delta = ctx->cfg.delta;
+  g.idh3 = 1.0 / (ctx->cfg.delta * L.h * L.h * L.h);
   g.dirmask = dirmask_of(ctx->cfg);
   g.cls = L.cls;
   g.code = L.code;

@@ -53,6 +53,7 @@ struct DGrid {
   int64_t px, py, fs;
   double h;
   double delta;     // stabilisation constant
+  double idh3;      // 1 / (delta h^3)
   unsigned dirmask; // bit f set: face f is homogeneous Dirichlet
   const uint8_t* cls;   // element classes [cz - cz0][cj][ci][t]
   const uint8_t* code;  // per-vertex code (plane layout of one field)
