@@ -50,6 +50,20 @@ CFG_INDEX = {"cfg1": 0, "cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4}
 OP_BYTES = {"apply": 65, "residual": 97, "vel_pass": 81, "p_pass1": 49, "p_pass2": 25}
 
 
+FORM_IDX = {"mod": 0, "sym": 1, "grad": 2}
+OP_IDX = {"apply": 0, "residual": 1, "vel_pass": 2, "p_pass1": 3, "p_pass2": 4}
+
+
+def ncu_traffic(kname):
+    """DRAM bytes per launch of kernel `kname` from the committed ncu summary, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            mb = json.load(f)["dram_MB_per_launch"].get(kname)
+        return None if mb is None else int(mb * 1e6)
+    except Exception:
+        return None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -341,9 +355,12 @@ def run_ours(args, cfg, world, rank, local):
         if n0 > 0:
             bytes_launch = OP_BYTES[dom] * V_own
             achieved = bytes_launch / (ms0 / n0 * 1e-3) / 1e9
-            roof = {"bound": "hbm", "kernel": f"k_stream<{dom}> level 0", "achieved": round(achieved, 1),
+            kname = f"k_stream<{FORM_IDX[args.form]}, {OP_IDX[dom]}>"
+            roof = {"bound": "hbm", "kernel": f"{kname} ({dom}, level 0)", "achieved": round(achieved, 1),
                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                    "traffic": None, "bytes_per_launch": bytes_launch, "launches_level0": n0,
+                    "traffic": ncu_traffic(kname), "traffic_source": "profiles/ncu_traffic.json (ncu --set full, "
+                    "dram__bytes_read.sum + dram__bytes_write.sum per launch, bytes)",
+                    "bytes_per_launch": bytes_launch, "launches_level0": n0,
                     "avg_launch_ms": ms0 / n0,
                     "share_of_step": round(prof[dom][1] / sum(step_ms), 4)}
     ops_ms = {k: round(v[1] / args.steps, 3) for k, v in prof.items() if v[0]}
@@ -430,7 +447,7 @@ def run_ours(args, cfg, world, rank, local):
                 "clocks": clk,
                 "e2e": {"value": e2e_ms_v * 1e-3 / dofs, "unit": "s/DoF", "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h)},
-                "gpu_launches": int(launches // max(args.steps, 1)),
+                "gpu_launches": int(launches),
                 "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     ctx.close()

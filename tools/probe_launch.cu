@@ -16,6 +16,13 @@ __global__ void k_chain3(const double* __restrict__ a, double* __restrict__ b, c
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n) { int i1 = __ldg(idx + t); int i2 = __ldg(idx + i1); b[t] = a[i2] + 1.0; }
 }
+// the same with programmatic dependent launch: index math before the wait
+__global__ void k_chain3_pdl(const double* a, double* b, const int* idx, int n) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (t < n) { int i1 = idx[t]; int i2 = idx[i1]; b[t] = a[i2] + 1.0; }
+}
 int main() {
   setvbuf(stdout, nullptr, _IONBF, 0);
   double *a, *b; int* idx;
@@ -27,7 +34,7 @@ int main() {
   const int R = 400;
   for (int n : {729, 4913, 35937, 274625}) {
     const int nb = (n + 127) / 128;
-    for (int kind = 0; kind < 4; ++kind) {
+    for (int kind = 0; kind < 5; ++kind) {
       cudaGraph_t gr; cudaGraphExec_t ge;
       cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed);
       for (int r = 0; r < R; ++r) {
@@ -35,6 +42,15 @@ int main() {
         if (kind == 1) k_copy<<<nb, 128, 0, s>>>((r & 1) ? b : a, (r & 1) ? a : b, n);
         if (kind == 2) k_copy_big<<<nb, 128, 0, s>>>(B, n);
         if (kind == 3) k_chain3<<<nb, 128, 0, s>>>(a, b, idx, n);
+        if (kind == 4) {
+          cudaLaunchConfig_t lc{};
+          lc.gridDim = dim3(nb); lc.blockDim = dim3(128); lc.stream = s;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          at[0].val.programmaticStreamSerializationAllowed = 1;
+          lc.attrs = at; lc.numAttrs = 1;
+          cudaLaunchKernelEx(&lc, k_chain3_pdl, (const double*)a, b, (const int*)idx, n);
+        }
       }
       cudaStreamEndCapture(s, &gr);
       cudaGraphInstantiate(&ge, gr, 0);
@@ -44,7 +60,7 @@ int main() {
       cudaEventRecord(e1, s);
       cudaEventSynchronize(e1);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
-      static const char* nm[] = {"empty", "copy", "copy_bigparam", "chain3"};
+      static const char* nm[] = {"empty", "copy", "copy_bigparam", "chain3", "chain3_pdl"};
       printf("n=%7d %-14s %.3f us per kernel in graph\n", n, nm[kind], ms * 1e3 / R);
       cudaGraphExecDestroy(ge); cudaGraphDestroy(gr);
     }
