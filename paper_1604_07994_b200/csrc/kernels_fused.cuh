@@ -50,28 +50,6 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, int M) {
   }
 }
 
-// the 15 Kuhn offsets (0, +-d, d in {0,1}^3 \ 0) as 27-point indices
-__host__ __device__ constexpr int kq_dx(int q) { return q == 0 ? 0 : (q & 1 ? 1 : -1) * (((q - 1) / 2 + 1) & 1); }
-__host__ __device__ constexpr int kq_dy(int q) { return q == 0 ? 0 : (q & 1 ? 1 : -1) * ((((q - 1) / 2 + 1) >> 1) & 1); }
-__host__ __device__ constexpr int kq_dz(int q) { return q == 0 ? 0 : (q & 1 ? 1 : -1) * ((((q - 1) / 2 + 1) >> 2) & 1); }
-constexpr int NQ = 15;
-constexpr bool kq_table_ok() {
-  // the 15 offsets are distinct and exactly the Kuhn pattern
-  int seen[27] = {};
-  for (int q = 0; q < NQ; ++q) {
-    const int dx = kq_dx(q), dy = kq_dy(q), dz = kq_dz(q);
-    if (!((dx >= 0 && dy >= 0 && dz >= 0) || (dx <= 0 && dy <= 0 && dz <= 0))) return false;
-    const int o = (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
-    if (seen[o]++) return false;
-  }
-  return true;
-}
-static_assert(kq_table_ok(), "Kuhn offset table");
-
-// explicit stencil of a row: S[r][q][c] (r, c: u1,u2,u3,p), the entries of K,
-// then the inverse diagonals 1/A_00, 1/A_11, 1/A_22, 1/C (Gauss-Seidel)
-constexpr int EXPL = 4 * NQ * 4 + 4;
-
 // one thread per (explicit row, offset q, column field c): row_generic applied to
 // the unit vector at (vertex + offset q, field c)
 template <int FORM>
@@ -147,9 +125,6 @@ __device__ __forceinline__ void fvertex(const DGrid& g, int t, int& i, int& j, i
 __device__ __forceinline__ int fidx(const DGrid& g, int i, int j, int k) {
   return (k - g.z0 + 1) * (int)g.py + (j + 1) * (int)g.px + (i + 1);
 }
-__device__ __forceinline__ int qoff(const DGrid& g, int q) {
-  return kq_dx(q) + kq_dy(q) * (int)g.px + kq_dz(q) * (int)g.py;
-}
 
 // the 15-point neighbourhood of padded index o (NF = 4: u1,u2,u3,p; NF = 1: p)
 template <int NF, bool COH>
@@ -182,8 +157,6 @@ __device__ __forceinline__ void c_trunc_nb(const double nb[NQ][4], int i, int j,
 }
 __device__ __forceinline__ constexpr bool q_axis(int q) { return q == 0 || q == 1 || q == 2 || q == 3 || q == 4 || q == 7 || q == 8; }
 __device__ __forceinline__ constexpr int q_o27(int q) { return (kq_dz(q) + 1) * 9 + (kq_dy(q) + 1) * 3 + (kq_dx(q) + 1); }
-// colour-1 vertex: its colour-0 Kuhn neighbours are those at an odd offset sum
-__device__ __forceinline__ constexpr bool q_odd(int q) { return ((kq_dx(q) + kq_dy(q) + kq_dz(q)) & 1) != 0; }
 
 // rows of K at an owned vertex from the gathered neighbourhood.  ROWS: 1 velocity
 // rows (A, B^T), 2 pressure row (B, -C), 3 both; PONLY: the pressure row of C on

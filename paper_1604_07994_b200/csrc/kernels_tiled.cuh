@@ -481,6 +481,114 @@ __device__ __forceinline__ void list_row(const DGrid& g, const StreamArgs& a, in
   }
 }
 
+// ---- list rows by explicit stencils: 16 lanes per row ------------------------------
+// The Gamma rows of a tiled level carry their explicit 4x4-block stencils
+// (k_assemble_explicit, "explicit interface stencils").  Lane q < 15 of a
+// row's 16-lane group takes Kuhn offset q: it loads the neighbour's 4 fields (masked:
+// velocity 0 at Dirichlet / outside, pressure 0 outside -- level-0 inputs are the
+// caller's vectors) and its 16 stencil entries, forms its part of the 4 row outputs;
+// a 16-lane xor reduction sums them and lane 0 writes (same results as list_row).
+constexpr int LX_NT = 128;
+template <int FORM, int OP>
+__global__ void __launch_bounds__(LX_NT) k_listx(DGrid g, StreamArgs a, const double* __restrict__ S0) {
+  const int gt = blockIdx.x * LX_NT + threadIdx.x;
+  const int e = gt >> 4, q = gt & 15;
+  if (e >= a.nlist) return;  // whole 16-lane groups retire together
+  const int t = __ldg(a.list + e);
+  const int nx = g.n + 1;
+  const int k = g.z0 + t / (nx * nx);
+  const int rr = t % (nx * nx);
+  const int i = rr % nx, j = rr / nx;
+  const int64_t o = vidx(g, i, j, k);
+  const bool dir = is_dirichlet(g, i, j, k);
+  const double* S = S0 + (int64_t)e * EXPL;
+  // which rows / columns this OP needs
+  constexpr bool VROWS = OP == OP_APPLY || OP == OP_RESID || OP == OP_VEL;
+  constexpr bool PROW = OP != OP_VEL;
+  constexpr bool UCOL = OP != OP_P2;
+  const bool c0 = ((i + j + k) & 1) == 0;  // pressure colour 0
+  bool act = true;
+  if (OP == OP_VEL) act = ((i + j + k) & (a.ncolors - 1)) == a.color && !dir;
+  if (OP == OP_P2) act = !c0;
+  double py[4] = {0.0, 0.0, 0.0, 0.0};
+  if (act && q < NQ) {
+    const int dx = kq_dx(q), dy = kq_dy(q), dz = kq_dz(q);
+    const int xi = i + dx, yj = j + dy, zk = k + dz;
+    const int n = g.n;
+    const bool in = xi >= 0 && yj >= 0 && zk >= 0 && xi <= n && yj <= n && zk <= n;
+    const int64_t oc = o + dx + dy * g.px + dz * g.py;
+    double u[3] = {0.0, 0.0, 0.0}, p = 0.0;
+    if (UCOL) {
+      const unsigned dm = g.dirmask;
+      const bool dv = !in || ((dm & 1u) && xi == 0) || ((dm & 2u) && xi == n) || ((dm & 4u) && yj == 0) ||
+                      ((dm & 8u) && yj == n) || ((dm & 16u) && zk == 0) || ((dm & 32u) && zk == n);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double v = __ldg(a.inU + c * g.fs + oc);
+        u[c] = dv ? 0.0 : v;
+      }
+    }
+    {
+      const double v = __ldg(a.inP + oc);
+      // P2: the masked T of R11 -- colour-0 neighbours only (odd offset sums)
+      p = (in && (OP != OP_P2 || ((dx + dy + dz) & 1))) ? v : 0.0;
+    }
+    if (VROWS) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const double2 s01 = __ldg(reinterpret_cast<const double2*>(S + (r * NQ + q) * 4));
+        const double2 s23 = __ldg(reinterpret_cast<const double2*>(S + (r * NQ + q) * 4 + 2));
+        const bool wA = OP == OP_VEL || OP == OP_RESID || (a.blocks & BLK_A);
+        const bool wT = OP == OP_VEL || OP == OP_RESID || (a.blocks & BLK_BT);
+        double v = 0.0;
+        if (wA) v = fma(s01.x, u[0], fma(s01.y, u[1], s23.x * u[2]));
+        if (wT) v = fma(s23.y, p, v);
+        py[r] = v;
+      }
+    }
+    if (PROW) {
+      const double2 s23 = __ldg(reinterpret_cast<const double2*>(S + (3 * NQ + q) * 4 + 2));
+      const bool wB = OP == OP_RESID || OP == OP_P1 || (OP == OP_APPLY && (a.blocks & BLK_B));
+      const bool wC = OP != OP_APPLY || (a.blocks & BLK_C);
+      double v = 0.0;
+      if (wB && UCOL) {
+        const double2 s01 = __ldg(reinterpret_cast<const double2*>(S + (3 * NQ + q) * 4));
+        v = fma(s01.x, u[0], fma(s01.y, u[1], s23.x * u[2]));
+      }
+      if (wC) v = fma(s23.y, p, v);
+      py[3] = v;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    if ((r < 3 && VROWS) || (r == 3 && PROW))
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) py[r] += __shfl_xor_sync(0xffffffffu, py[r], off);
+  if (q != 0) return;
+  const double* inv = S + 4 * NQ * 4;  // 1/A_00, 1/A_11, 1/A_22, 1/C
+  if (OP == OP_APPLY || OP == OP_RESID) {
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      double v = (f < 3 && dir) ? 0.0 : py[f];
+      if (OP == OP_RESID) v = (f < 3 && dir) ? 0.0 : __ldg(a.aux + f * g.fs + o) - py[f];
+      a.out[f * g.fs + o] = v;
+    }
+  } else if (OP == OP_VEL) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double uc = dir ? 0.0 : __ldg(a.inU + c * g.fs + o);
+      a.out[c * g.fs + o] = act ? fma(__ldg(a.aux + c * g.fs + o) - py[c], __ldg(inv + c), uc) : uc;
+    }
+  } else if (OP == OP_P1) {
+    const double r = py[3] - __ldg(a.aux + o);
+    a.out[o] = c0 ? r * __ldg(inv + 3) : r;
+  } else {
+    const double T = __ldg(a.inP + o);
+    const double d = c0 ? T : (T + py[3]) * __ldg(inv + 3);
+    a.out[o] += a.omega * d;
+  }
+}
+
 constexpr int LIST_NT = 128;
 template <int FORM, int OP>
 __global__ void __launch_bounds__(LIST_NT) k_list(DGrid g, StreamArgs a) {
@@ -904,6 +1012,7 @@ inline size_t stream_smem(int op) {
 struct ListView {
   const int32_t* list;
   int n;
+  const double* S;                // explicit stencils of the list rows [n][EXPL] (nullptr: element loop)
   cudaStream_t side;              // list kernel runs here, concurrently (nullptr: same stream)
   cudaEvent_t ev_fork, ev_join;
 };
@@ -967,7 +1076,10 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
       return false;
   }
   k_stream<FORM, OP><<<dim3(grid), NT, sm, st>>>(mU, mP, g, a);
-  if (do_list) k_list<FORM, OP><<<(lv.n + LIST_NT - 1) / LIST_NT, LIST_NT, 0, fork ? lv.side : st>>>(g, a);
+  if (do_list) {
+    if (lv.S) k_listx<FORM, OP><<<(unsigned)(((int64_t)lv.n * 16 + LX_NT - 1) / LX_NT), LX_NT, 0, fork ? lv.side : st>>>(g, a, lv.S);
+    else k_list<FORM, OP><<<(lv.n + LIST_NT - 1) / LIST_NT, LIST_NT, 0, fork ? lv.side : st>>>(g, a);
+  }
   if (fork) {
     if (cudaEventRecord(lv.ev_join, lv.side) != cudaSuccess || cudaStreamWaitEvent(st, lv.ev_join, 0) != cudaSuccess)
       return false;

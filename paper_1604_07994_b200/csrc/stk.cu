@@ -40,6 +40,7 @@ struct Level {
   int32_t* xrows = nullptr; // explicit rows (owned linear indices)
   double* S = nullptr;      // explicit stencils [slot][EXPL]
   int64_t nexpl = 0;
+  double* Slist = nullptr;  // explicit stencils of the list rows [nirr][EXPL] (tiled levels)
 };
 
 // event-timed profile of the kernels launched while enabled (stk_profile_*)
@@ -282,7 +283,8 @@ void slab_partition(int n, int nc, int P, int rank, std::vector<SlabLevel>& out)
 // ---- level operations ------------------------------------------------------
 
 ListView lview(const stk_ctx* ctx, const Level& L) {
-  return ListView{L.list, (int)L.nirr, ctx->side, ctx->ev_fork, ctx->ev_join};
+  static const bool xl = !getenv("STK_LIST_EXPLICIT") || atoi(getenv("STK_LIST_EXPLICIT"));
+  return ListView{L.list, (int)L.nirr, xl ? L.Slist : nullptr, ctx->side, ctx->ev_fork, ctx->ev_join};
 }
 
 bool use_tiled(const stk_ctx* ctx, const Level& L) {
@@ -1202,6 +1204,18 @@ stk_status stk_assemble(stk_ctx* ctx) {
     ST(launched(ctx));
     CK(cudaStreamSynchronize(ctx->stream));
     cudaFree(lc);
+    // explicit stencils of the list rows, for k_listx
+    cudaFree(L.Slist);
+    L.Slist = nullptr;
+    CK(cudaMalloc(&L.Slist, sizeof(double) * EXPL * L.nirr));
+    const unsigned nbx = nblocks((int64_t)L.nirr * NQ * 4);
+    DGrid gl = dgrid(ctx, L);
+    switch (ctx->cfg.form) {
+      case FORM_MOD: k_assemble_explicit<FORM_MOD><<<nbx, kThreads, 0, ctx->stream>>>(gl, L.list, (int)L.nirr, L.Slist); break;
+      case FORM_SYM: k_assemble_explicit<FORM_SYM><<<nbx, kThreads, 0, ctx->stream>>>(gl, L.list, (int)L.nirr, L.Slist); break;
+      default: k_assemble_explicit<FORM_GRAD><<<nbx, kThreads, 0, ctx->stream>>>(gl, L.list, (int)L.nirr, L.Slist); break;
+    }
+    ST(launched(ctx));
   }
   // constant subdomain stencils for the tiled kernels
   for (int l = 0; l < ctx->nlev; ++l) {
@@ -1542,6 +1556,7 @@ stk_status stk_destroy(stk_ctx* ctx) {
     cudaFree(L.slot);
     cudaFree(L.xrows);
     cudaFree(L.S);
+    cudaFree(L.Slist);
   }
   cudaFree(ctx->fbar);
   cudaFree(ctx->fprog);
