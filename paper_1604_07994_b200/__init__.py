@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstk.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("STK_LIBNAME", "libstk.so"))  # in-tree build variants only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
