@@ -41,6 +41,7 @@ struct Level {
   double* S = nullptr;      // explicit stencils [slot][EXPL]
   int64_t nexpl = 0;
   double* Slist = nullptr;  // explicit stencils of the list rows [nirr][EXPL] (tiled levels)
+  size_t cap_list = 0, cap_Slist = 0, cap_slot = 0, cap_xrows = 0, cap_S = 0;
 };
 
 // event-timed profile of the kernels launched while enabled (stk_profile_*)
@@ -107,6 +108,9 @@ struct stk_ctx {
   int rl = -1;      // first row level, -1: none
   int fgrid = 0;
   unsigned long long* fbar = nullptr;     // grid-barrier counters (one per prefix size)
+  size_t cap_cdofs = 0, cap_cK = 0, cap_cG = 0, cap_cfac = 0;
+  unsigned long long* dcnt = nullptr;     // assembly counters (nlev + 1)
+  std::vector<int64_t> graph_sig;         // what the captured coarse graph depends on
   FPhase* fprog = nullptr;                // phase program of the fused V-cycle (device)
   int fnph = 0, fgrid_used = 0;
   double* cfac = nullptr;                 // Gauss-Jordan column factors
@@ -165,6 +169,19 @@ constexpr int kThreads = 256;
     stk_status s_ = (call);           \
     if (s_ != STK_OK) return s_;      \
   } while (0)
+
+// device buffer with capacity: reallocated only when it must grow, so re-assembly
+// (new viscosity, same grid) keeps every pointer the captured coarse graph holds
+template <class T>
+bool ensure(T*& p, size_t& cap, size_t count) {
+  if (p && count <= cap) return true;
+  cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  if (cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)) != cudaSuccess) return false;
+  cap = std::max<size_t>(count, 1);
+  return true;
+}
 
 stk_status launched(stk_ctx* ctx) {
   ctx->launches++;
@@ -878,14 +895,7 @@ stk_status fused_setup(stk_ctx* ctx) {
 // on held whole by this rank; explicit stencils of its non-regular rows
 stk_status fused_assemble(stk_ctx* ctx) {
   ctx->fl = -1;
-  for (auto& L : ctx->lev) {
-    cudaFree(L.slot);
-    cudaFree(L.xrows);
-    cudaFree(L.S);
-    L.slot = L.xrows = nullptr;
-    L.S = nullptr;
-    L.nexpl = 0;
-  }
+  for (auto& L : ctx->lev) L.nexpl = 0;
   ctx->rl = -1;
   if (ctx->kernel_mode != 1) return STK_OK;
   int rl = -1;
@@ -903,13 +913,12 @@ stk_status fused_assemble(stk_ctx* ctx) {
       fl = l;
     }
   ST(assemble_stencils(ctx->stream) ? STK_OK : STK_ECUDA);
-  unsigned long long* dcnt;
-  CK(cudaMalloc(&dcnt, sizeof(unsigned long long)));
+  if (!ctx->dcnt) CK(cudaMalloc(&ctx->dcnt, sizeof(unsigned long long) * (ctx->nlev + 1)));
+  unsigned long long* dcnt = ctx->dcnt + ctx->nlev;
   for (int l = rl; l < ctx->nlev; ++l) {
     Level& L = ctx->lev[l];
     const int64_t V = owned_vertices(L);
-    CK(cudaMalloc(&L.slot, sizeof(int32_t) * L.fs));
-    CK(cudaMalloc(&L.xrows, sizeof(int32_t) * V));
+    if (!ensure(L.slot, L.cap_slot, (size_t)L.fs) || !ensure(L.xrows, L.cap_xrows, (size_t)V)) return STK_ENOMEM;
     CK(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long), ctx->stream));
     k_build_explicit<<<nblocks(V), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), L.slot, L.xrows, dcnt);
     ST(launched(ctx));
@@ -918,7 +927,7 @@ stk_status fused_assemble(stk_ctx* ctx) {
     CK(cudaStreamSynchronize(ctx->stream));
     L.nexpl = (int64_t)c;
     if (c == 0) continue;
-    CK(cudaMalloc(&L.S, sizeof(double) * EXPL * c));
+    if (!ensure(L.S, L.cap_S, (size_t)EXPL * c)) return STK_ENOMEM;
     const unsigned nb = nblocks((int64_t)c * NQ * 4);
     DGrid g = dgrid(ctx, L);
     switch (ctx->cfg.form) {
@@ -929,7 +938,6 @@ stk_status fused_assemble(stk_ctx* ctx) {
     ST(launched(ctx));
   }
   CK(cudaStreamSynchronize(ctx->stream));
-  cudaFree(dcnt);
   ctx->rl = rl;
   if (fl < 0) return STK_OK;
   // phase program (the V-cycle of op_vcycle / op_uzawa restricted to levels fl..)
@@ -977,9 +985,7 @@ stk_status fused_assemble(stk_ctx* ctx) {
     prog[k].barM = (int16_t)(next ? std::max<int>(prog[k].m, next) : 0);
     gmax = std::max<int>(gmax, prog[k].m);
   }
-  cudaFree(ctx->fprog);
-  ctx->fprog = nullptr;
-  CK(cudaMalloc(&ctx->fprog, sizeof(FPhase) * prog.size()));
+  if (!ctx->fprog) CK(cudaMalloc(&ctx->fprog, sizeof(FPhase) * FPH_MAX));
   CK(cudaMemcpy(ctx->fprog, prog.data(), sizeof(FPhase) * prog.size(), cudaMemcpyHostToDevice));
   ctx->fnph = (int)prog.size();
   ctx->fgrid_used = gmax;
@@ -1162,7 +1168,6 @@ stk_status stk_set_viscosity(stk_ctx* ctx, const uint8_t* elem_class, const doub
 
 stk_status stk_assemble(stk_ctx* ctx) {
   ST(check(ctx, 1));
-  drop_graphs(ctx);
   // coarse classes
   for (int l = 1; l < ctx->nlev; ++l) {
     Level& F = ctx->lev[l - 1];
@@ -1177,8 +1182,8 @@ stk_status stk_assemble(stk_ctx* ctx) {
     }
   }
   // classification
-  unsigned long long* dcnt;
-  CK(cudaMalloc(&dcnt, sizeof(unsigned long long) * ctx->nlev));
+  if (!ctx->dcnt) CK(cudaMalloc(&ctx->dcnt, sizeof(unsigned long long) * (ctx->nlev + 1)));
+  unsigned long long* dcnt = ctx->dcnt;
   CK(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * ctx->nlev, ctx->stream));
   for (int l = 0; l < ctx->nlev; ++l) {
     Level& L = ctx->lev[l];
@@ -1188,26 +1193,18 @@ stk_status stk_assemble(stk_ctx* ctx) {
   std::vector<unsigned long long> cnt(ctx->nlev);
   CK(cudaMemcpyAsync(cnt.data(), dcnt, sizeof(unsigned long long) * ctx->nlev, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  cudaFree(dcnt);
   for (int l = 0; l < ctx->nlev; ++l) ctx->lev[l].nirr = (int64_t)cnt[l];
   // compact list rows of the tiled levels (the list role of k_stream)
   for (int l = 0; l < ctx->nlev; ++l) {
     Level& L = ctx->lev[l];
-    cudaFree(L.list);
-    L.list = nullptr;
     if (L.n < 64 || L.nirr == 0) continue;
-    CK(cudaMalloc(&L.list, sizeof(int32_t) * L.nirr));
-    unsigned long long* lc;
-    CK(cudaMalloc(&lc, sizeof(unsigned long long)));
+    if (!ensure(L.list, L.cap_list, (size_t)L.nirr)) return STK_ENOMEM;
+    unsigned long long* lc = ctx->dcnt + ctx->nlev;
     CK(cudaMemsetAsync(lc, 0, sizeof(unsigned long long), ctx->stream));
     k_build_list<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), L.list, lc);
     ST(launched(ctx));
-    CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(lc);
     // explicit stencils of the list rows, for k_listx
-    cudaFree(L.Slist);
-    L.Slist = nullptr;
-    CK(cudaMalloc(&L.Slist, sizeof(double) * EXPL * L.nirr));
+    if (!ensure(L.Slist, L.cap_Slist, (size_t)EXPL * L.nirr)) return STK_ENOMEM;
     const unsigned nbx = nblocks((int64_t)L.nirr * NQ * 4);
     DGrid gl = dgrid(ctx, L);
     switch (ctx->cfg.form) {
@@ -1246,12 +1243,9 @@ stk_status stk_assemble(stk_ctx* ctx) {
   ctx->cN = (int)dofs.size();
   ctx->cN1 = ctx->cN + (gauge ? 1 : 0);
   const int N1 = ctx->cN1;
-  cudaFree(ctx->cdofs);
-  cudaFree(ctx->cK);
-  cudaFree(ctx->cG);
-  CK(cudaMalloc(&ctx->cdofs, sizeof(int32_t) * ctx->cN));
-  CK(cudaMalloc(&ctx->cK, sizeof(double) * N1 * N1));
-  CK(cudaMalloc(&ctx->cG, sizeof(double) * N1 * N1));
+  if (!ensure(ctx->cdofs, ctx->cap_cdofs, (size_t)ctx->cN) || !ensure(ctx->cK, ctx->cap_cK, (size_t)N1 * N1) ||
+      !ensure(ctx->cG, ctx->cap_cG, (size_t)N1 * N1))
+    return STK_ENOMEM;
   CK(cudaMemcpyAsync(ctx->cdofs, dofs.data(), sizeof(int32_t) * ctx->cN, cudaMemcpyHostToDevice, ctx->stream));
   DGrid g = dgrid(ctx, L);
   const unsigned nb = nblocks((int64_t)N1 * N1);
@@ -1264,9 +1258,7 @@ stk_status stk_assemble(stk_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->cstatus, 0, sizeof(int), ctx->stream));
   ST(fused_setup(ctx));  // grid size + barrier words (used by the coarse inverse too)
   {
-    cudaFree(ctx->cfac);
-    ctx->cfac = nullptr;
-    CK(cudaMalloc(&ctx->cfac, sizeof(double) * N1));
+    if (!ensure(ctx->cfac, ctx->cap_cfac, (size_t)N1)) return STK_ENOMEM;
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(std::min(ctx->fgrid, std::max(1, (N1 * N1 + 255) / 256)));
     lc.blockDim = dim3(256);
@@ -1287,6 +1279,15 @@ stk_status stk_assemble(stk_ctx* ctx) {
     ctx->err = "coarse-level matrix is singular";
     return STK_ECUDA;
   }
+  // keep the captured coarse graph when nothing it depends on changed (pointers,
+  // list / explicit-row counts, kernel selection); the data behind them is updated
+  std::vector<int64_t> sig = {ctx->kernel_mode, ctx->rl, ctx->fl, ctx->row_n, ctx->fuse_n, ctx->cN, ctx->cN1,
+                              (int64_t)ctx->cdofs, (int64_t)ctx->cG, (int64_t)ctx->fprog, ctx->fnph};
+  for (auto& Lv : ctx->lev)
+    for (int64_t v : {(int64_t)Lv.list, Lv.nirr, (int64_t)Lv.Slist, (int64_t)Lv.slot, (int64_t)Lv.S, Lv.nexpl})
+      sig.push_back(v);
+  if (sig != ctx->graph_sig) drop_graphs(ctx);
+  ctx->graph_sig = sig;
   ctx->state = 2;
   return STK_OK;
 }
@@ -1559,6 +1560,7 @@ stk_status stk_destroy(stk_ctx* ctx) {
     cudaFree(L.Slist);
   }
   cudaFree(ctx->fbar);
+  cudaFree(ctx->dcnt);
   cudaFree(ctx->fprog);
   cudaFree(ctx->cfac);
   cudaFree(ctx->cdofs);
