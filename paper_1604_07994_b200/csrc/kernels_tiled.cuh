@@ -229,8 +229,6 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait3() { asm volatile("cp.async.wait_group 3;" ::: "memory"); }
-constexpr int AUXD = 3;  // per-row data (aux fields, codes) is fetched AUXD rows ahead
 
 struct StreamArgs {
   double* out;          // y (APPLY), r (RESID), u_out (VEL, 3 fields), T (P1), p (P2)
@@ -767,7 +765,7 @@ __global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP ==
       smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);  // 1 KB aligned TMA destinations
   double* ring = reinterpret_cast<double*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + RING * SLOT * sizeof(double));
-  double* auxb = reinterpret_cast<double*>(bars + RING);  // [AUXD][NA][NT] per-thread aux ring
+  double* auxb = reinterpret_cast<double*>(bars + RING);  // [2][NA][NT] per-thread aux double buffer
 
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int ntx = g.n / TX;
@@ -863,52 +861,36 @@ __global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP ==
     }
     release();
     int64_t o = vidx(g, i, j, kb);  // output row of the current iteration
-    const int64_t ob = o;           // row kb (base of the look-ahead addresses)
-    const int klast = kb + M - 3;   // last output row of the item
-    // per-row data AUXD rows ahead: the aux fields through a cp.async ring (one
-    // group per row; rows past the item commit empty groups, so no copy is in
-    // flight into a buffer when the next item starts), the codes into registers
-    // whose queue slots are renamed by the 3-way unroll of the row loop below
+    uint8_t code_nx = __ldg(g.code + o);
+    // aux of row kb into buffer ab (cp.async group); each body prefetches the next row
     const double* auxsrc = OP == OP_P2 ? a.out : a.aux;
-    auto aux_issue = [&](int k_, int buf) {
-      if (k_ <= klast) {
-        const int64_t orow = ob + (int64_t)(k_ - kb) * g.py;
+    auto aux_issue = [&](int64_t orow, int buf) {
 #pragma unroll
-        for (int f = 0; f < NA; ++f) cp_async8(auxb + (buf * NA + f) * NT + threadIdx.x, auxsrc + f * g.fs + orow);
-      }
+      for (int f = 0; f < NA; ++f) cp_async8(auxb + (buf * NA + f) * NT + threadIdx.x, auxsrc + f * g.fs + orow);
       cp_async_commit();
     };
-    struct CQ { uint8_t c, x, y, xy; };
-    auto code_load = [&](CQ& q, int k_) {
-      k_ = min(k_, klast);
-      const uint8_t* cp = g.code + ob + (int64_t)(k_ - kb) * g.py;
-      q.c = __ldg(cp);
-      q.x = ex_x ? __ldg(cp + 1) : (uint8_t)0xFF;
-      q.y = ex_y ? __ldg(cp + g.px) : (uint8_t)0xFF;
-      q.xy = ex_c ? __ldg(cp + g.px + 1) : (uint8_t)0xFF;
-    };
-    CQ Q0, Q1, Q2;
-    code_load(Q0, kb);
-    code_load(Q1, kb + 1);
-    code_load(Q2, kb + 2);
-    if (NA > 0) {
-      aux_issue(kb, 0);
-      aux_issue(kb + 1, 1);
-      aux_issue(kb + 2, 2);
-    }
+    int ab = 0;
+    if (NA > 0) aux_issue(o, ab);
 
-    auto body = [&](int m, Acc& acc0, Acc& acc1, Acc& acc2, int bi, CQ& cq) {
+    auto body = [&](int m, Acc& acc0, Acc& acc1, Acc& acc2) {
       const int k = kb1 + m - 1;  // output finished in this iteration
       acc2.zero();
-      const uint8_t code = cq.c;
-      uint8_t cxy[3] = {cq.x, cq.y, cq.xy};
-      code_load(cq, k + AUXD);
+      // per-output data of row k, staged with plane k (previous slot, landed)
+      const uint8_t code = code_nx;           // loaded one iteration ahead
+      code_nx = __ldg(g.code + o + g.py);     // next row (the code array holds the halo planes)
+      uint8_t cxy[3] = {0xFF, 0xFF, 0xFF};
+      if (any_ex) {
+        if (ex_x) cxy[0] = __ldg(g.code + o + 1);
+        if (ex_y) cxy[1] = __ldg(g.code + o + g.px);
+        if (ex_c) cxy[2] = __ldg(g.code + o + g.px + 1);
+      }
       double aux[4] = {0, 0, 0, 0};
       if (NA > 0) {
-        aux_issue(k + AUXD, bi);      // this row's buffer is re-armed for row k + AUXD ...
-        cp_async_wait3();             // ... after row k's group has landed (3 newer groups may pend)
+        aux_issue(o + g.py, ab ^ 1);  // next row (the slab holds the halo planes)
+        cp_async_wait1();             // this row's group has landed
 #pragma unroll
-        for (int f = 0; f < NA; ++f) aux[OP == OP_RESID || OP == OP_VEL ? f : 3] = auxb[(bi * NA + f) * NT + threadIdx.x];
+        for (int f = 0; f < NA; ++f) aux[OP == OP_RESID || OP == OP_VEL ? f : 3] = auxb[(ab * NA + f) * NT + threadIdx.x];
+        ab ^= 1;
       }
       const double* pl = wait_plane();
       // plane P is output P-1's z+1 plane, output P's own plane, output P+1's z-1 plane
@@ -940,12 +922,12 @@ __global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP ==
     };
     int m = 2;
     for (; m + 2 < M; m += 3) {
-      body(m, R2, R0, R1, 0, Q0);
-      body(m + 1, R0, R1, R2, 1, Q1);
-      body(m + 2, R1, R2, R0, 2, Q2);
+      body(m, R2, R0, R1);
+      body(m + 1, R0, R1, R2);
+      body(m + 2, R1, R2, R0);
     }
-    if (m < M) body(m, R2, R0, R1, 0, Q0);
-    if (m + 1 < M) body(m + 1, R0, R1, R2, 1, Q1);
+    if (m < M) body(m, R2, R0, R1);
+    if (m + 1 < M) body(m + 1, R0, R1, R2);
   }
 }
 
@@ -1023,7 +1005,7 @@ inline bool assemble_stencils(cudaStream_t st) {
 }
 
 inline size_t stream_smem(int op) {
-  return 1024 + RING * slot_doubles(op) * sizeof(double) + RING * sizeof(uint64_t) + AUXD * n_aux(op) * NT * sizeof(double);
+  return 1024 + RING * slot_doubles(op) * sizeof(double) + RING * sizeof(uint64_t) + 2 * n_aux(op) * NT * sizeof(double);
 }
 
 // the irregular-row list of a level (built by stk_assemble)
