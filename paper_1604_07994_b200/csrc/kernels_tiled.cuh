@@ -133,6 +133,13 @@ __constant__ double st_B[3][27];        // pressure row, velocity column b
 __constant__ double st_C[27];
 
 enum { OP_APPLY = 0, OP_RESID = 1, OP_VEL = 2, OP_P1 = 3, OP_P2 = 4 };
+#ifndef STK_TMA_FENCE
+#define STK_TMA_FENCE 1
+#endif
+#ifndef STK_TMA_PREFETCH
+#define STK_TMA_PREFETCH 0
+#endif
+
 
 // one thread: unit stencils of the interior vertex by summing the element
 // matrices of its 24 incident tetrahedra (the "constant subdomain stencils")
@@ -242,6 +249,7 @@ struct StreamArgs {
   int color, ncolors;   // VEL
   double omega;         // P2
   int ux0, uy0, uz0;    // velocity tensor-map origin (vertex coordinates)
+  unsigned long long* trace;  // debug (STK_STREAM_TRACE): per-CTA cycle counters, else nullptr
 };
 
 // in-plane offsets of one streamed plane: (0,0) (1,0) (-1,0) (0,1) (0,-1) (1,1) (-1,-1)
@@ -785,6 +793,10 @@ __global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP ==
   if (threadIdx.x == 0) {
     for (int s = 0; s < RING; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#if STK_TMA_PREFETCH
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapU) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapP) : "memory");
+#endif
   }
   __syncthreads();
   // Producer (thread 0): the planes of this CTA's items, items blockIdx.x + q G,
@@ -799,7 +811,9 @@ __global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP ==
     if (!pvalid) return;
     const int s = pS % RING;
     const int P = pkb - 1 + pp;
+#if STK_TMA_FENCE
     fence_proxy_async();
+#endif
     mbar_expect_tx(&bars[s], TX_BYTES);
     double* dst = ring + s * SLOT;
     if (NF == 4) {
@@ -822,14 +836,26 @@ __global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP ==
     for (int q = 0; q < RING - 2; ++q) issue_next();  // consumer iteration S stages plane S+RING-2
 
   int S = 0;  // consumer: global plane sequence number
+  // debug trace (a.trace != nullptr): cycles in the plane waits, the per-plane
+  // barrier and the producer's issue, for thread 0 and for the last warp's lane 0
+  const bool trc = a.trace != nullptr && (threadIdx.x == 0 || threadIdx.x == NT - 32);
+  unsigned long long tw = 0, ts = 0, ti = 0, t_start = trc ? clock64() : 0;
   auto wait_plane = [&]() -> const double* {
     const int s = S % RING;
+    const unsigned long long c0 = trc ? clock64() : 0;
     mbar_wait(&bars[s], (S / RING) & 1);
+    if (trc) tw += clock64() - c0;
     return ring + s * SLOT;
   };
   auto release = [&]() {  // all reads of plane S-2 are done: stage a new plane into its slot
+    const unsigned long long c0 = trc ? clock64() : 0;
     __syncthreads();
+    const unsigned long long c1 = trc ? clock64() : 0;
     if (threadIdx.x == 0) issue_next();
+    if (trc) {
+      ts += c1 - c0;
+      ti += clock64() - c1;
+    }
     ++S;
   };
   const int i_ofs = tx, j_ofs = ty;
@@ -920,14 +946,33 @@ __global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP ==
       release();
       o += g.py;
     };
-    int m = 2;
-    for (; m + 2 < M; m += 3) {
-      body(m, R2, R0, R1);
-      body(m + 1, R0, R1, R2);
-      body(m + 2, R1, R2, R0);
+    if constexpr (OP != OP_VEL) {
+      // one body instance, the accumulators rotate by register moves: 3x less code
+      // (measured faster for these OPs; the velocity pass keeps the 3-way unroll)
+#pragma unroll 1
+      for (int m = 2; m < M; ++m) {
+        body(m, R2, R0, R1);
+        R2 = R0;
+        R0 = R1;
+      }
+    } else {
+      int m = 2;
+      for (; m + 2 < M; m += 3) {
+        body(m, R2, R0, R1);
+        body(m + 1, R0, R1, R2);
+        body(m + 2, R1, R2, R0);
+      }
+      if (m < M) body(m, R2, R0, R1);
+      if (m + 1 < M) body(m + 1, R0, R1, R2);
     }
-    if (m < M) body(m, R2, R0, R1);
-    if (m + 1 < M) body(m + 1, R0, R1, R2);
+  }
+  if (trc) {
+    unsigned long long* d = a.trace + (blockIdx.x * 2 + (threadIdx.x ? 1 : 0)) * 5;
+    d[0] = clock64() - t_start;
+    d[1] = tw;
+    d[2] = ts;
+    d[3] = ti;
+    d[4] = S;
   }
 }
 
@@ -1075,7 +1120,21 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
     if (cudaEventRecord(lv.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(lv.side, lv.ev_fork, 0) != cudaSuccess)
       return false;
   }
+  static const bool trace = getenv("STK_STREAM_TRACE") && atoi(getenv("STK_STREAM_TRACE"));
+  static unsigned long long* tbuf = nullptr;
+  if (trace && !tbuf) cudaMallocManaged(&tbuf, sizeof(unsigned long long) * 4096 * 10);
+  a.trace = trace ? tbuf : nullptr;
   k_stream<FORM, OP><<<dim3(grid), NT, sm, st>>>(mU, mP, g, a);
+  if (trace) {  // debug: mean per-CTA cycle split of this launch
+    cudaStreamSynchronize(st);
+    double tot[2][5] = {};
+    for (int b = 0; b < grid; ++b)
+      for (int r = 0; r < 2; ++r)
+        for (int q = 0; q < 5; ++q) tot[r][q] += (double)tbuf[(b * 2 + r) * 5 + q] / grid;
+    fprintf(stderr, "k_stream<%d,%d> n=%d grid=%d kc=%d planes/CTA %.1f | thread0: total %.0f wait %.0f sync %.0f issue %.0f"
+            " | last warp: total %.0f wait %.0f sync %.0f (cycles)\n", FORM, OP, g.n, grid, kc, tot[0][4], tot[0][0],
+            tot[0][1], tot[0][2], tot[0][3], tot[1][0], tot[1][1], tot[1][2]);
+  }
   if (do_list) {
     if (lv.S) k_listx<FORM, OP><<<(unsigned)(((int64_t)lv.n * 16 + LX_NT - 1) / LX_NT), LX_NT, 0, fork ? lv.side : st>>>(g, a, lv.S);
     else k_list<FORM, OP><<<(lv.n + LIST_NT - 1) / LIST_NT, LIST_NT, 0, fork ? lv.side : st>>>(g, a);
