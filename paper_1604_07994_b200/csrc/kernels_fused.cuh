@@ -18,6 +18,7 @@
 // Also: k_gauss_jordan_coop, the coarsest-level inverse (setup) with the same
 // grid barrier (the single-CTA version spent ~11 ms in L2 round trips).
 #pragma once
+#include <cooperative_groups.h>
 #include "kernels_generic.cuh"
 #include "kernels_tiled.cuh"
 
@@ -801,6 +802,120 @@ __global__ void __launch_bounds__(256, 1) k_mg_fused(const __grid_constant__ Fus
     if (P.barM > 0 && (int)blockIdx.x < P.barM) grid_barrier(A.bar, P.barM);
     if (tr) A.trace[ph] = globaltimer();
   }
+}
+
+// ---- coarsest-level inverse on one thread-block cluster (distributed shared memory) ----
+// In-place Gauss-Jordan with partial pivoting: CTA r of the GJC-CTA cluster holds rows
+// [r R, (r+1) R) of the N x N matrix in its shared memory.  Per column k: every CTA
+// offers its best pivot candidate (|A[i][k]|, i >= k) to CTA 0 -> cluster barrier ->
+// every CTA picks the pivot row p (ties -> lowest index), reads row p remotely and
+// forms the scaled pivot row (A[k][k] -> 1/piv, others / piv) in its own buffer; the
+// owner of p keeps a copy of row k -> cluster barrier -> the owners write the swapped
+// rows, every CTA eliminates its other rows with its pivot-row copy.  Two cluster
+// barriers per column (the grid version needed two grid barriers plus a one-CTA
+// pivot phase).  Column interchanges are undone at the end (Numerical-Recipes order).
+constexpr int GJC = 8, GJC_NT = 256;
+inline size_t gj_cluster_smem(int N) {
+  const int R = (N + GJC - 1) / GJC;
+  return sizeof(double) * ((size_t)R * N + 2 * (size_t)N + GJC) + sizeof(int) * (GJC + N + 8);
+}
+__global__ void __cluster_dims__(GJC, 1, 1) __launch_bounds__(GJC_NT)
+    k_gauss_jordan_cluster(const double* __restrict__ K, double* __restrict__ G, int N, int* status) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int R = (N + GJC - 1) / GJC;
+  const int r0 = rank * R, r1 = min(N, r0 + R);
+  extern __shared__ double gsm[];
+  double* A = gsm;                    // [R][N] own rows
+  double* prow = A + (size_t)R * N;   // scaled pivot row (private copy)
+  double* keep = prow + N;            // old row k (owner of row p only)
+  double* cval = keep + N;            // [GJC] candidates (CTA 0's copy is read)
+  int* cidx = reinterpret_cast<int*>(cval + GJC);
+  int* perm = cidx + GJC;             // [N] pivot rows
+  __shared__ double wv[GJC_NT / 32];
+  __shared__ int wi[GJC_NT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < (r1 - r0) * N; e += GJC_NT) A[e] = K[(size_t)(r0 + e / N) * N + e % N];
+  __syncthreads();
+  for (int k = 0; k < N; ++k) {
+    // local pivot candidate among own rows i >= k
+    double bv = -1.0;
+    int bi = N;
+    for (int i = max(r0, k) + tid; i < r1; i += GJC_NT) {
+      const double v = fabs(A[(size_t)(i - r0) * N + k]);
+      if (v > bv) { bv = v; bi = i; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { wv[wid] = bv; wi[wid] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < GJC_NT / 32; ++w)
+        if (wv[w] > bv || (wv[w] == bv && wi[w] < bi)) { bv = wv[w]; bi = wi[w]; }
+      double* rv = cl.map_shared_rank(cval, 0);
+      int* ri = cl.map_shared_rank(cidx, 0);
+      rv[rank] = bv;
+      ri[rank] = bi;
+    }
+    cl.sync();
+    // global pivot (every CTA reads CTA 0's candidates)
+    int p;
+    {
+      const double* rv = cl.map_shared_rank(cval, 0);
+      const int* ri = cl.map_shared_rank(cidx, 0);
+      double gv = rv[0];
+      p = ri[0];
+      for (int q = 1; q < GJC; ++q)
+        if (rv[q] > gv || (rv[q] == gv && ri[q] < p)) { gv = rv[q]; p = ri[q]; }
+      if (tid == 0 && rank == 0 && !(gv > 0.0)) *status = 1;
+    }
+    const int op = p / R, ok = k / R;
+    const double* rowp = cl.map_shared_rank(A, op) + (size_t)(p - op * R) * N;
+    const double piv = rowp[k];
+    const double ipiv = 1.0 / piv;
+    for (int j = tid; j < N; j += GJC_NT) prow[j] = j == k ? ipiv : rowp[j] * ipiv;
+    if (rank == op && p != k) {
+      const double* rowk = cl.map_shared_rank(A, ok) + (size_t)(k - ok * R) * N;
+      for (int j = tid; j < N; j += GJC_NT) keep[j] = rowk[j];
+    }
+    if (tid == 0) perm[k] = p;
+    cl.sync();
+    if (rank == ok)
+      for (int j = tid; j < N; j += GJC_NT) A[(size_t)(k - r0) * N + j] = prow[j];
+    if (rank == op && p != k)
+      for (int j = tid; j < N; j += GJC_NT) A[(size_t)(p - r0) * N + j] = keep[j];
+    __syncthreads();
+    // eliminate column k from the own rows i != k: A[i][k] -> -f / piv, A[i][j] -= f prow[j]
+    const int nr = r1 - r0;
+    for (int w = wid; w < nr; w += GJC_NT / 32) {
+      const int i = r0 + w;
+      if (i == k) continue;
+      double* ai = A + (size_t)w * N;
+      const double f = ai[k];
+      if (f == 0.0) continue;
+      for (int j = lane; j < N; j += 32) ai[j] = j == k ? -f * prow[k] : fma(-f, prow[j], ai[j]);
+    }
+    __syncthreads();
+  }
+  // undo the row interchanges as column interchanges, in reverse order
+  for (int k = N - 1; k >= 0; --k) {
+    const int p = perm[k];
+    if (p == k) continue;
+    for (int w = tid; w < r1 - r0; w += GJC_NT) {
+      double* ai = A + (size_t)w * N;
+      const double t = ai[k];
+      ai[k] = ai[p];
+      ai[p] = t;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < (r1 - r0) * N; e += GJC_NT) G[(size_t)(r0 + e / N) * N + e % N] = A[e];
+  cl.sync();  // no CTA leaves while its shared memory may still be read remotely
 }
 
 // ---- coarsest-level inverse: Gauss-Jordan with partial pivoting, grid-parallel ----

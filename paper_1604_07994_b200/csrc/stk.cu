@@ -1257,7 +1257,13 @@ stk_status stk_assemble(stk_ctx* ctx) {
   ST(launched(ctx));
   CK(cudaMemsetAsync(ctx->cstatus, 0, sizeof(int), ctx->stream));
   ST(fused_setup(ctx));  // grid size + barrier words (used by the coarse inverse too)
-  {
+  static const bool gj_grid = getenv("STK_GJ_GRID") && atoi(getenv("STK_GJ_GRID"));
+  const size_t gsm = gj_cluster_smem(N1);
+  if (!gj_grid && gsm <= 220 * 1024) {  // one 8-CTA cluster, matrix in distributed shared memory
+    CK(cudaFuncSetAttribute(k_gauss_jordan_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+    k_gauss_jordan_cluster<<<GJC, GJC_NT, gsm, ctx->stream>>>(ctx->cK, ctx->cG, N1, ctx->cstatus);
+    ST(launched(ctx));
+  } else {
     if (!ensure(ctx->cfac, ctx->cap_cfac, (size_t)N1)) return STK_ENOMEM;
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(std::min(ctx->fgrid, std::max(1, (N1 * N1 + 255) / 256)));
