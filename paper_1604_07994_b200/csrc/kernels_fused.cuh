@@ -509,20 +509,20 @@ __device__ __forceinline__ double seg_sum(double v) {
 // the interior B on the zero-extended velocity and the truncated C (c_trunc).
 // Returns the group sums in y[0..3] on every lane of the group.
 template <int FORM, int ROWS, bool PONLY, int LPR>
-__device__ __forceinline__ void row_lanes(const FLevel& L, int o, int i, int j, int k, uint8_t code, int sub,
-                                          const double* U, const double* P, double y[4]) {
+__device__ __forceinline__ void row_lanes(const FLevel& L, const MuTab& M, int o, int i, int j, int k, uint8_t code,
+                                          int slot, int sub, const double* U, const double* P, double y[4]) {
   const DGrid& g = L.g;
   double py[4] = {0.0, 0.0, 0.0, 0.0};
   const bool expl = code >= 0x40;
-  const double* S = expl ? L.S + (int64_t)__ldg(L.slot + o) * EXPL : nullptr;
+  const double* S = expl ? L.S + (int64_t)slot * EXPL : nullptr;
   const double h = g.h;
   const bool interior = i > 0 && j > 0 && k > 0 && i < g.n && j < g.n && k < g.n;
   double sA = 0.0, sB = h * h, sC = 0.0, cw = 0.0;
   int wq[3] = {0, 0, 0};
   double diag = 0.0;
   if (!expl) {
-    sA = mu_of(g, code) * h;
-    sC = g.delta * h * h * h * imu_of(g, code);
+    sA = M.mu[code] * h;
+    sC = g.delta * h * h * h * M.imu[code];
     if (!interior && (ROWS & 2)) {
       const int X0 = i >= 1, X1 = i <= g.n - 1, Y0 = j >= 1, Y1 = j <= g.n - 1, Z0 = k >= 1, Z1 = k <= g.n - 1;
       wq[0] = 2 * (Y1 & Z1) + (Y0 & Z1) + (Y1 & Z0) + 2 * (Y0 & Z0);
@@ -598,19 +598,19 @@ __device__ __forceinline__ void row_lanes(const FLevel& L, int o, int i, int j, 
 }
 // inverse diagonals of a row (lane 0 of the group)
 template <int FORM>
-__device__ __forceinline__ void row_inv_diag(const FLevel& L, int o, int i, int j, int k, uint8_t code, double iA[3],
-                                             double& iC) {
+__device__ __forceinline__ void row_inv_diag(const FLevel& L, const MuTab& M, int o, int i, int j, int k, uint8_t code,
+                                             int slot, double iA[3], double& iC) {
   const DGrid& g = L.g;
   if (code >= 0x40) {
-    const double* S = L.S + (int64_t)__ldg(L.slot + o) * EXPL + 4 * NQ * 4;
+    const double* S = L.S + (int64_t)slot * EXPL + 4 * NQ * 4;
     iA[0] = __ldg(S);
     iA[1] = __ldg(S + 1);
     iA[2] = __ldg(S + 2);
     iC = __ldg(S + 3);
     return;
   }
-  const double h = g.h, mu = mu_of(g, code);
-  const double ia = imu_of(g, code) * (double)g.n * 6.0;
+  const double h = g.h, mu = M.mu[code];
+  const double ia = M.imu[code] * (double)g.n * 6.0;
   iA[0] = ia * (1.0 / KS<0, FORM, 0, 0, 0, 0, 0>::v);
   iA[1] = ia * (1.0 / KS<0, FORM, 1, 1, 0, 0, 0>::v);
   iA[2] = ia * (1.0 / KS<0, FORM, 2, 2, 0, 0, 0>::v);
@@ -631,7 +631,8 @@ __device__ __forceinline__ void row_inv_diag(const FLevel& L, int o, int i, int 
 // flow up to the shuffles (the row index is uniform within the group)
 template <int FORM, int OP, int LPR>
 __global__ void __launch_bounds__(ROW_NT) k_rowl(const __grid_constant__ FLevel L, const __grid_constant__ FLevel L2,
-                                                 const double* uin, double* uout, int color, int nc, double omega) {
+                                                 const double* uin, double* uout, int color, int nc, double omega,
+                                                 const __grid_constant__ MuTab M) {
   const int gt = blockIdx.x * ROW_NT + threadIdx.x;
   const int sub = gt & (LPR - 1);
   const DGrid& g = L.g;
@@ -675,23 +676,27 @@ __global__ void __launch_bounds__(ROW_NT) k_rowl(const __grid_constant__ FLevel 
       return;
     }
     const uint8_t code = __ldg(g.code + o);
+    const int slot = __ldg(L.slot + o);  // independent of code: one round trip for both
+    const int c3 = sub < 3 ? sub : 0;
+    const double bown = __ldg(L.b + c3 * g.fs + o), uown = __ldg(uin + c3 * g.fs + o);  // issued early
     double y[4];
-    row_lanes<FORM, 1, false, LPR>(L, o, i, j, k, code, sub, uin, L.x + 3 * g.fs, y);
+    row_lanes<FORM, 1, false, LPR>(L, M, o, i, j, k, code, slot, sub, uin, L.x + 3 * g.fs, y);
     if (sub < 3) {
       double iA[3], iC;
-      row_inv_diag<FORM>(L, o, i, j, k, code, iA, iC);
+      row_inv_diag<FORM>(L, M, o, i, j, k, code, slot, iA, iC);
       const double yv = sub == 0 ? y[0] : sub == 1 ? y[1] : y[2];
       const double ia = sub == 0 ? iA[0] : sub == 1 ? iA[1] : iA[2];
-      uout[sub * g.fs + o] = fma(__ldg(L.b + sub * g.fs + o) - yv, ia, __ldg(uin + sub * g.fs + o));
+      uout[sub * g.fs + o] = fma(bown - yv, ia, uown);
     }
   } else if (OP == FPH_P1) {  // T = (B u - C p - g) / C_ii on colour 0, unscaled on colour 1
     const uint8_t code = __ldg(g.code + o);
+    const int slot = __ldg(L.slot + o);
     double y[4];
-    row_lanes<FORM, 2, false, LPR>(L, o, i, j, k, code, sub, L.x, L.x + 3 * g.fs, y);
+    row_lanes<FORM, 2, false, LPR>(L, M, o, i, j, k, code, slot, sub, L.x, L.x + 3 * g.fs, y);
     if (sub == 0) {
       const double r = y[3] - __ldg(L.b + 3 * g.fs + o);
       double iA[3], iC = 1.0;
-      if (((i + j + k) & 1) == 0) row_inv_diag<FORM>(L, o, i, j, k, code, iA, iC);
+      if (((i + j + k) & 1) == 0) row_inv_diag<FORM>(L, M, o, i, j, k, code, slot, iA, iC);
       L.r[3 * g.fs + o] = ((i + j + k) & 1) == 0 ? r * iC : r;
     }
   } else if (OP == FPH_P2) {  // p += omega delta
@@ -702,17 +707,19 @@ __global__ void __launch_bounds__(ROW_NT) k_rowl(const __grid_constant__ FLevel 
       return;
     }
     const uint8_t code = __ldg(g.code + o);
+    const int slot = __ldg(L.slot + o);
     double y[4];
-    row_lanes<FORM, 2, true, LPR>(L, o, i, j, k, code, sub, nullptr, T, y);
+    row_lanes<FORM, 2, true, LPR>(L, M, o, i, j, k, code, slot, sub, nullptr, T, y);
     if (sub == 0) {
       double iA[3], iC;
-      row_inv_diag<FORM>(L, o, i, j, k, code, iA, iC);
+      row_inv_diag<FORM>(L, M, o, i, j, k, code, slot, iA, iC);
       p[o] = fma(omega, (__ldg(T + o) + y[3]) * iC, p[o]);
     }
   } else if (OP == FPH_RES) {  // r = b - K x
     const uint8_t code = __ldg(g.code + o);
+    const int slot = __ldg(L.slot + o);
     double y[4];
-    row_lanes<FORM, 3, false, LPR>(L, o, i, j, k, code, sub, L.x, L.x + 3 * g.fs, y);
+    row_lanes<FORM, 3, false, LPR>(L, M, o, i, j, k, code, slot, sub, L.x, L.x + 3 * g.fs, y);
     if (sub < 4) {
       const bool dir = is_dirichlet(g, i, j, k);
       const double yv = sub == 0 ? y[0] : sub == 1 ? y[1] : sub == 2 ? y[2] : y[3];

@@ -97,6 +97,7 @@ struct stk_ctx {
   double* cG = nullptr;
   int* cstatus = nullptr;
   double* d_mu = nullptr;   // per-class mu_k (256) and 1/mu_k (256)
+  MuTab mutab{};            // the same table, passed to the row kernels as a parameter
   cudaStream_t side = nullptr;            // list-row kernels run here, forked from `stream`
   cudaStream_t cap = nullptr;             // capture stream for the coarse-level CUDA graph
   cudaGraphExec_t coarse_exec = nullptr;  // levels >= 1 of the V-cycle (fixed internal buffers)
@@ -512,9 +513,9 @@ void launch_rowl(stk_ctx* ctx, const FLevel& F, const FLevel& F2, int64_t rows, 
   const int nc = ctx->cfg.ncolors_u;
   const double om = ctx->cfg.omega;
   switch (ctx->cfg.form) {
-    case FORM_MOD: k_rowl<FORM_MOD, OP, LPR><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om); break;
-    case FORM_SYM: k_rowl<FORM_SYM, OP, LPR><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om); break;
-    default: k_rowl<FORM_GRAD, OP, LPR><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om); break;
+    case FORM_MOD: k_rowl<FORM_MOD, OP, LPR><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om, ctx->mutab); break;
+    case FORM_SYM: k_rowl<FORM_SYM, OP, LPR><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om, ctx->mutab); break;
+    default: k_rowl<FORM_GRAD, OP, LPR><<<nb, ROW_NT, 0, ctx->stream>>>(F, F2, uin, uout, color, nc, om, ctx->mutab); break;
   }
 }
 // lanes per row: 16 (one Kuhn offset per lane) on the latency-bound small levels,
@@ -1157,6 +1158,8 @@ stk_status stk_set_viscosity(stk_ctx* ctx, const uint8_t* elem_class, const doub
   ctx->class_mu.assign(class_mu, class_mu + nclass);
   CK(cudaMemcpyAsync(ctx->d_mu, mu, sizeof(mu), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->d_mu + 256, imu, sizeof(imu), cudaMemcpyHostToDevice, ctx->stream));
+  memcpy(ctx->mutab.mu, mu, sizeof(mu));
+  memcpy(ctx->mutab.imu, imu, sizeof(imu));
   Level& L = ctx->lev[0];
   const size_t ncls = (size_t)(L.cz1 - L.cz0) * L.n * L.n * 6;
   CK(cudaMemcpyAsync(L.cls, elem_class, ncls, cudaMemcpyHostToDevice, ctx->stream));
@@ -1292,6 +1295,11 @@ stk_status stk_assemble(stk_ctx* ctx) {
   for (auto& Lv : ctx->lev)
     for (int64_t v : {(int64_t)Lv.list, Lv.nirr, (int64_t)Lv.Slist, (int64_t)Lv.slot, (int64_t)Lv.S, Lv.nexpl})
       sig.push_back(v);
+  for (int q = 0; q < 256; ++q) {  // the row kernels take the class table by value
+    int64_t b;
+    memcpy(&b, &ctx->mutab.mu[q], 8);
+    sig.push_back(b);
+  }
   if (sig != ctx->graph_sig) drop_graphs(ctx);
   ctx->graph_sig = sig;
   ctx->state = 2;

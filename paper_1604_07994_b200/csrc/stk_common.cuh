@@ -61,6 +61,11 @@ struct DGrid {
 };
 
 __device__ __forceinline__ double mu_of(const DGrid& g, int cl) { return __ldg(g.mu + cl); }
+// the same per-class table as a kernel parameter (constant bank): the latency-bound
+// coarse-level row kernels read mu without a dependent L2 round trip
+struct MuTab {
+  double mu[256], imu[256];
+};
 __device__ __forceinline__ double imu_of(const DGrid& g, int cl) { return __ldg(g.mu + 256 + cl); }
 
 __device__ __forceinline__ int64_t vidx(const DGrid& g, int i, int j, int k) {
