@@ -524,8 +524,9 @@ template <int OP>
 stk_status launch_row(stk_ctx* ctx, const FLevel& F, const FLevel& F2, int64_t rows, const double* uin = nullptr,
                       double* uout = nullptr, int color = 0) {
   static const int env = getenv("STK_ROW_LPR") ? atoi(getenv("STK_ROW_LPR")) : 0;
-  const int lpr = env == 1 || env == 4 || env == 16 ? env : (rows <= 40000 ? 16 : 4);
+  const int lpr = env == 1 || env == 4 || env == 8 || env == 16 ? env : (rows <= 40000 ? 16 : 4);
   if (lpr == 16) launch_rowl<OP, 16>(ctx, F, F2, rows, uin, uout, color);
+  else if (lpr == 8) launch_rowl<OP, 8>(ctx, F, F2, rows, uin, uout, color);
   else if (lpr == 4) launch_rowl<OP, 4>(ctx, F, F2, rows, uin, uout, color);
   else {
     const unsigned nb = (unsigned)((rows + ROW_NT - 1) / ROW_NT);
