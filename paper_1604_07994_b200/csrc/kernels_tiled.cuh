@@ -760,7 +760,17 @@ __device__ __forceinline__ void finish_row(const DGrid& g, const StreamArgs& a, 
 }
 
 template <int FORM, int OP>
-__global__ void __launch_bounds__(NT, (OP == OP_APPLY || OP == OP_RESID || OP == OP_VEL) ? 2 : 3)
+// register budget: 2 (apply / residual / velocity) or 3 (pressure passes) CTAs per SM
+// with a little left over, so that one k_listx CTA (128 threads x 32 registers) can
+// run next to the persistent stream CTAs and the Gamma rows overlap the stream
+// (the residual spills at 120 and keeps 128: measured)
+#ifndef STK_REGS_AR
+#define STK_REGS_AR 120
+#endif
+#ifndef STK_REGS_P
+#define STK_REGS_P 80
+#endif
+__global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_VEL) ? STK_REGS_AR : STK_REGS_P)
     k_stream(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapP,
              DGrid g,
              StreamArgs a) {
