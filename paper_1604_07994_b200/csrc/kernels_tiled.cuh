@@ -1190,6 +1190,41 @@ inline bool launch_vel_pass_tiled(int form, DGrid g, const ListView& lv, const d
   a.ncolors = ncolors;
   return launch_stream<OP_VEL>(form, g, uin, p, lv, a, st);
 }
+// The second pass of the middle colour pair of the symmetric sweep (colours
+// 0..nc-1, nc-1..0; R12) repeats the relaxation of the same colour.  A regular row of
+// the mod / grad forms couples only to other colours (7-point A) and to
+// its own component (diagonal centre block), so the repeat reproduces it exactly in
+// exact arithmetic (to rounding in fp64): only the rows that couple within the colour
+// change -- the list rows (Gamma_12, Gamma_F) and the isoviscous traction-face rows
+// (truncated stencils).  So: u_out = u_in (one device copy of the 3 velocity fields),
+// then those rows are relaxed from u_in (k_listx over the "repeat list").  Same
+// result as the full pass up to rounding.
+template <int FORM>
+bool launch_vel_repeat_t(const DGrid& g, const ListView& lv, const double* uin, const double* p, const double* b,
+                         double* uout, int color, int ncolors, cudaStream_t st) {
+  if (cudaMemcpyAsync(uout, uin, sizeof(double) * 3 * g.fs, cudaMemcpyDeviceToDevice, st) != cudaSuccess) return false;
+  if (lv.n == 0) return true;
+  StreamArgs a{};
+  a.out = uout;
+  a.aux = b;
+  a.color = color;
+  a.ncolors = ncolors;
+  a.inU = uin;
+  a.inP = p;
+  a.list = lv.list;
+  a.nlist = lv.n;
+  if (lv.S) k_listx<FORM, OP_VEL><<<(unsigned)(((int64_t)lv.n * 16 + LX_NT - 1) / LX_NT), LX_NT, 0, st>>>(g, a, lv.S);
+  else k_list<FORM, OP_VEL><<<(lv.n + LIST_NT - 1) / LIST_NT, LIST_NT, 0, st>>>(g, a);
+  return true;
+}
+inline bool launch_vel_repeat(int form, DGrid g, const ListView& lv, const double* uin, const double* p,
+                              const double* b, double* uout, int color, int ncolors, cudaStream_t st) {
+  switch (form) {
+    case FORM_MOD: return launch_vel_repeat_t<FORM_MOD>(g, lv, uin, p, b, uout, color, ncolors, st);
+    case FORM_SYM: return launch_vel_repeat_t<FORM_SYM>(g, lv, uin, p, b, uout, color, ncolors, st);
+    default: return launch_vel_repeat_t<FORM_GRAD>(g, lv, uin, p, b, uout, color, ncolors, st);
+  }
+}
 inline bool launch_p_pass1_tiled(int form, DGrid g, const ListView& lv, const double* x, const double* gp, double* T,
                                  cudaStream_t st) {
   StreamArgs a{};

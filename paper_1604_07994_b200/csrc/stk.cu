@@ -42,6 +42,11 @@ struct Level {
   int64_t nexpl = 0;
   double* Slist = nullptr;  // explicit stencils of the list rows [nirr][EXPL] (tiled levels)
   size_t cap_list = 0, cap_Slist = 0, cap_slot = 0, cap_xrows = 0, cap_S = 0;
+  // repeat-pass rows (list rows + isoviscous traction-face rows) and their stencils
+  int32_t* rlist = nullptr;
+  double* Srl = nullptr;
+  int64_t nrl = 0;
+  size_t cap_rlist = 0, cap_Srl = 0;
 };
 
 // event-timed profile of the kernels launched while enabled (stk_profile_*)
@@ -381,7 +386,17 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
     double* uout = (pass & 1) ? x : tmp;
     ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, const_cast<double*>(uin), 0, 3, L.replicated));
     PScope ps(ctx, P_VEL, l);
-    if (tiled) {
+    static const bool repeat_env = !getenv("STK_VEL_REPEAT") || atoi(getenv("STK_VEL_REPEAT"));
+    // second pass of the middle colour pair: list + traction-face rows only (forms whose
+    // regular rows have a diagonal centre block: mod, grad; the sym centre block
+    // couples the 3 components of a vertex, so its repeat is not a no-op)
+    if (tiled && s == nc && repeat_env && ctx->cfg.form != FORM_SYM) {
+      ListView rv = lview(ctx, L);
+      rv.list = L.rlist;
+      rv.n = (int)L.nrl;
+      rv.S = L.Srl;
+      ST(launch_vel_repeat(ctx->cfg.form, g, rv, uin, p, b, uout, color, nc, ctx->stream) ? STK_OK : STK_EUNSUP);
+    } else if (tiled) {
       ST(launch_vel_pass_tiled(ctx->cfg.form, g, lview(ctx, L), uin, p, b, uout, color, nc, ctx->stream) ? STK_OK
                                                                                            : STK_EUNSUP);
     } else if (warp_rows(L)) {
@@ -1217,6 +1232,27 @@ stk_status stk_assemble(stk_ctx* ctx) {
       default: k_assemble_explicit<FORM_GRAD><<<nbx, kThreads, 0, ctx->stream>>>(gl, L.list, (int)L.nirr, L.Slist); break;
     }
     ST(launched(ctx));
+    // rows that couple within a colour (list rows + traction-face rows): the repeat pass
+    unsigned long long* tc = ctx->dcnt + ctx->nlev;
+    CK(cudaMemsetAsync(tc, 0, sizeof(unsigned long long), ctx->stream));
+    k_count_top<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), tc);
+    ST(launched(ctx));
+    unsigned long long ntop = 0;
+    CK(cudaMemcpyAsync(&ntop, tc, sizeof(ntop), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    L.nrl = L.nirr + (int64_t)ntop;
+    if (!ensure(L.rlist, L.cap_rlist, (size_t)L.nrl) || !ensure(L.Srl, L.cap_Srl, (size_t)EXPL * L.nrl))
+      return STK_ENOMEM;
+    CK(cudaMemsetAsync(tc, 0, sizeof(unsigned long long), ctx->stream));
+    k_build_list<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), L.rlist, tc, 1);
+    ST(launched(ctx));
+    const unsigned nbr = nblocks((int64_t)L.nrl * NQ * 4);
+    switch (ctx->cfg.form) {
+      case FORM_MOD: k_assemble_explicit<FORM_MOD><<<nbr, kThreads, 0, ctx->stream>>>(gl, L.rlist, (int)L.nrl, L.Srl); break;
+      case FORM_SYM: k_assemble_explicit<FORM_SYM><<<nbr, kThreads, 0, ctx->stream>>>(gl, L.rlist, (int)L.nrl, L.Srl); break;
+      default: k_assemble_explicit<FORM_GRAD><<<nbr, kThreads, 0, ctx->stream>>>(gl, L.rlist, (int)L.nrl, L.Srl); break;
+    }
+    ST(launched(ctx));
   }
   // constant subdomain stencils for the tiled kernels
   for (int l = 0; l < ctx->nlev; ++l) {
@@ -1294,7 +1330,8 @@ stk_status stk_assemble(stk_ctx* ctx) {
   std::vector<int64_t> sig = {ctx->kernel_mode, ctx->rl, ctx->fl, ctx->row_n, ctx->fuse_n, ctx->cN, ctx->cN1,
                               (int64_t)ctx->cdofs, (int64_t)ctx->cG, (int64_t)ctx->fprog, ctx->fnph};
   for (auto& Lv : ctx->lev)
-    for (int64_t v : {(int64_t)Lv.list, Lv.nirr, (int64_t)Lv.Slist, (int64_t)Lv.slot, (int64_t)Lv.S, Lv.nexpl})
+    for (int64_t v : {(int64_t)Lv.list, Lv.nirr, (int64_t)Lv.Slist, (int64_t)Lv.slot, (int64_t)Lv.S, Lv.nexpl,
+                      (int64_t)Lv.rlist, Lv.nrl, (int64_t)Lv.Srl})
       sig.push_back(v);
   for (int q = 0; q < 256; ++q) {  // the row kernels take the class table by value
     int64_t b;
@@ -1573,6 +1610,8 @@ stk_status stk_destroy(stk_ctx* ctx) {
     cudaFree(L.xrows);
     cudaFree(L.S);
     cudaFree(L.Slist);
+    cudaFree(L.rlist);
+    cudaFree(L.Srl);
   }
   cudaFree(ctx->fbar);
   cudaFree(ctx->dcnt);
