@@ -2,16 +2,20 @@
 //
 // Design:
 //  * List rows (interface Gamma_12, the traction boundary Gamma_F, vertices
-//    touching both kinds of faces) are evaluated by a second kernel, k_list:
-//    one row per thread by the cube-major element loop row_list (exact element
-//    formulas), reading the input from global memory (L2).  The two kernels
-//    write disjoint rows; k_list runs concurrently on a side stream forked from
-//    (and joined back into) the caller's stream (STK_LIST_FORK=0: serial).
+//    touching both kinds of faces) are evaluated by a second kernel, k_listx:
+//    16 lanes per row over the row's explicit 4x4-block stencils (assembled
+//    once per level from the element loop), reading the input from
+//    global memory (L2).  The two kernels write disjoint rows; k_listx runs on
+//    a side stream forked from (and joined back into) the caller's stream, and
+//    the stream kernels' register caps leave room for one of its CTAs per SM
+//    (STK_LIST_EXPLICIT=0: the per-thread element loop k_list instead;
+//    STK_LIST_FORK=0: serial).
 //  * A stream CTA owns a TX x TY column tile (i in [i0, i0+TX), j in
 //    [j0, j0+TY), i0+TX <= n) and a chunk of z-planes.  Each plane of the input
 //    fields, with a 1-vertex xy halo, is staged in shared memory by TMA boxes
 //    (cp.async.bulk.tensor.4d + mbarrier complete_tx), PREF planes ahead, in a
-//    ring of PREF+2 slots.  One __syncthreads per plane.
+//    ring of PREF+2 slots.  One __syncthreads per plane.  CTAs are persistent
+//    (one per resident slot) and take items (tile, z-chunk) round robin.
 //  * Plane-streaming accumulation: when plane P lands, every thread reads the
 //    7 in-plane points of its column once and adds their contributions to the
 //    rows of outputs P-1, P, P+1 of its column (the 15-point Kuhn stencil

@@ -50,7 +50,8 @@ struct Level {
 };
 
 // event-timed profile of the kernels launched while enabled (stk_profile_*)
-enum { P_APPLY = 0, P_RESID, P_VEL, P_P1, P_P2, P_RESTRICT, P_PROLONG, P_COARSE, P_REDUCE, P_KRYLOV, P_CGRAPH, P_FUSED, P_NOPS };
+enum { P_APPLY = 0, P_RESID, P_VEL, P_P1, P_P2, P_RESTRICT, P_PROLONG, P_COARSE, P_REDUCE, P_KRYLOV, P_CGRAPH, P_FUSED,
+       P_VREP, P_NOPS };
 struct ProfRec {
   int op, level;
   cudaEvent_t e0, e1;
@@ -385,12 +386,13 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
     const double* uin = (pass & 1) ? tmp : x;
     double* uout = (pass & 1) ? x : tmp;
     ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, const_cast<double*>(uin), 0, 3, L.replicated));
-    PScope ps(ctx, P_VEL, l);
     static const bool repeat_env = !getenv("STK_VEL_REPEAT") || atoi(getenv("STK_VEL_REPEAT"));
     // second pass of the middle colour pair: list + traction-face rows only (forms whose
     // regular rows have a diagonal centre block: mod, grad; the sym centre block
     // couples the 3 components of a vertex, so its repeat is not a no-op)
-    if (tiled && s == nc && repeat_env && ctx->cfg.form != FORM_SYM) {
+    const bool repeat = tiled && s == nc && repeat_env && ctx->cfg.form != FORM_SYM;
+    PScope ps(ctx, repeat ? P_VREP : P_VEL, l);
+    if (repeat) {
       ListView rv = lview(ctx, L);
       rv.list = L.rlist;
       rv.n = (int)L.nrl;
