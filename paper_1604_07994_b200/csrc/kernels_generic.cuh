@@ -381,14 +381,15 @@ __global__ void k_classify(DGrid g, uint8_t* __restrict__ code, unsigned long lo
 // compact list of the owned list rows (CODE_IRREGULAR), as owned linear indices
 // t = (k - z0) (n+1)^2 + j (n+1) + i; *cnt must be zeroed.  Order is irrelevant:
 // every row is evaluated independently.
-// (with_top: also the isoviscous traction-face rows, code 0x40 | k -- the rows whose
+// (top = 1: instead the isoviscous traction-face rows, code 0x40 | k -- the rows whose
 // truncated stencils couple within a colour, for the repeat pass of the smoother)
-__global__ void k_build_list(DGrid g, int32_t* __restrict__ list, unsigned long long* cnt, int with_top = 0) {
+__global__ void k_build_list(DGrid g, int32_t* __restrict__ list, unsigned long long* cnt, int top = 0) {
   int i, j, k;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (!owned_vertex(g, tid, i, j, k)) return;
   const uint8_t c = g.code[vidx(g, i, j, k)];
-  if (c == CODE_IRREGULAR || (with_top && c >= 0x40)) list[atomicAdd(cnt, 1ull)] = (int32_t)tid;
+  const bool take = top ? (c >= 0x40 && c != CODE_IRREGULAR) : c == CODE_IRREGULAR;
+  if (take) list[atomicAdd(cnt, 1ull)] = (int32_t)tid;
 }
 __global__ void k_count_top(DGrid g, unsigned long long* cnt) {
   int i, j, k;

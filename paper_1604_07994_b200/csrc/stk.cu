@@ -1215,26 +1215,15 @@ stk_status stk_assemble(stk_ctx* ctx) {
   CK(cudaMemcpyAsync(cnt.data(), dcnt, sizeof(unsigned long long) * ctx->nlev, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   for (int l = 0; l < ctx->nlev; ++l) ctx->lev[l].nirr = (int64_t)cnt[l];
-  // compact list rows of the tiled levels (the list role of k_stream)
+  // compact list rows of the tiled levels (the list role of k_stream): the Gamma rows
+  // first, then the isoviscous traction-face rows (which also couple within a colour:
+  // the repeat pass of the smoother takes both); one explicit stencil each
   for (int l = 0; l < ctx->nlev; ++l) {
     Level& L = ctx->lev[l];
-    if (L.n < 64 || L.nirr == 0) continue;
-    if (!ensure(L.list, L.cap_list, (size_t)L.nirr)) return STK_ENOMEM;
-    unsigned long long* lc = ctx->dcnt + ctx->nlev;
-    CK(cudaMemsetAsync(lc, 0, sizeof(unsigned long long), ctx->stream));
-    k_build_list<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), L.list, lc);
-    ST(launched(ctx));
-    // explicit stencils of the list rows, for k_listx
-    if (!ensure(L.Slist, L.cap_Slist, (size_t)EXPL * L.nirr)) return STK_ENOMEM;
-    const unsigned nbx = nblocks((int64_t)L.nirr * NQ * 4);
-    DGrid gl = dgrid(ctx, L);
-    switch (ctx->cfg.form) {
-      case FORM_MOD: k_assemble_explicit<FORM_MOD><<<nbx, kThreads, 0, ctx->stream>>>(gl, L.list, (int)L.nirr, L.Slist); break;
-      case FORM_SYM: k_assemble_explicit<FORM_SYM><<<nbx, kThreads, 0, ctx->stream>>>(gl, L.list, (int)L.nirr, L.Slist); break;
-      default: k_assemble_explicit<FORM_GRAD><<<nbx, kThreads, 0, ctx->stream>>>(gl, L.list, (int)L.nirr, L.Slist); break;
-    }
-    ST(launched(ctx));
-    // rows that couple within a colour (list rows + traction-face rows): the repeat pass
+    L.list = nullptr;
+    L.Slist = nullptr;
+    L.nrl = 0;
+    if (L.n < 64) continue;
     unsigned long long* tc = ctx->dcnt + ctx->nlev;
     CK(cudaMemsetAsync(tc, 0, sizeof(unsigned long long), ctx->stream));
     k_count_top<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), tc);
@@ -1243,18 +1232,27 @@ stk_status stk_assemble(stk_ctx* ctx) {
     CK(cudaMemcpyAsync(&ntop, tc, sizeof(ntop), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     L.nrl = L.nirr + (int64_t)ntop;
+    if (L.nrl == 0) continue;
     if (!ensure(L.rlist, L.cap_rlist, (size_t)L.nrl) || !ensure(L.Srl, L.cap_Srl, (size_t)EXPL * L.nrl))
       return STK_ENOMEM;
     CK(cudaMemsetAsync(tc, 0, sizeof(unsigned long long), ctx->stream));
-    k_build_list<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), L.rlist, tc, 1);
+    k_build_list<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), L.rlist, tc, 0);
+    ST(launched(ctx));
+    CK(cudaMemsetAsync(tc, 0, sizeof(unsigned long long), ctx->stream));
+    k_build_list<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), L.rlist + L.nirr, tc, 1);
     ST(launched(ctx));
     const unsigned nbr = nblocks((int64_t)L.nrl * NQ * 4);
+    DGrid gl = dgrid(ctx, L);
     switch (ctx->cfg.form) {
       case FORM_MOD: k_assemble_explicit<FORM_MOD><<<nbr, kThreads, 0, ctx->stream>>>(gl, L.rlist, (int)L.nrl, L.Srl); break;
       case FORM_SYM: k_assemble_explicit<FORM_SYM><<<nbr, kThreads, 0, ctx->stream>>>(gl, L.rlist, (int)L.nrl, L.Srl); break;
       default: k_assemble_explicit<FORM_GRAD><<<nbr, kThreads, 0, ctx->stream>>>(gl, L.rlist, (int)L.nrl, L.Srl); break;
     }
     ST(launched(ctx));
+    if (L.nirr > 0) {  // the Gamma rows are the head of the repeat list
+      L.list = L.rlist;
+      L.Slist = L.Srl;
+    }
   }
   // constant subdomain stencils for the tiled kernels
   for (int l = 0; l < ctx->nlev; ++l) {
@@ -1604,14 +1602,12 @@ stk_status stk_destroy(stk_ctx* ctx) {
   for (auto& L : ctx->lev) {
     cudaFree(L.cls);
     cudaFree(L.code);
-    cudaFree(L.list);
     cudaFree(L.x);
     cudaFree(L.b);
     cudaFree(L.r);
     cudaFree(L.slot);
     cudaFree(L.xrows);
     cudaFree(L.S);
-    cudaFree(L.Slist);
     cudaFree(L.rlist);
     cudaFree(L.Srl);
   }
