@@ -229,7 +229,10 @@ DGrid dgrid(const stk_ctx* ctx, const Level& L) {
 int64_t owned_vertices(const Level& L) { return (int64_t)(L.n + 1) * (L.n + 1) * L.nzl; }
 unsigned nblocks(int64_t work) { return (unsigned)((work + kThreads - 1) / kThreads); }
 // small levels (n <= 16): one warp per row (latency-bound; kernels_generic.cuh *_gw)
-bool warp_rows(const Level& L) { return L.n <= 16; }
+bool warp_rows(const Level& L) {
+  static const int gw_n = getenv("STK_GW_N") ? atoi(getenv("STK_GW_N")) : 16;
+  return L.n <= gw_n;
+}
 unsigned nblocks_gw(const Level& L) { return (unsigned)((owned_vertices(L) * 32 + GW_NT - 1) / GW_NT); }
 
 bool has_traction(const stk_config& c) {
