@@ -870,17 +870,26 @@ __global__ void __cluster_dims__(GJC, 1, 1) __launch_bounds__(GJC_NT)
       ri[rank] = bi;
     }
     cl.sync();
-    // global pivot (every CTA reads CTA 0's candidates)
-    int p;
-    {
+    // global pivot: lanes 0..GJC-1 of warp 0 read CTA 0's candidates in parallel
+    __shared__ int psh;
+    if (wid == 0) {
       const double* rv = cl.map_shared_rank(cval, 0);
       const int* ri = cl.map_shared_rank(cidx, 0);
-      double gv = rv[0];
-      p = ri[0];
-      for (int q = 1; q < GJC; ++q)
-        if (rv[q] > gv || (rv[q] == gv && ri[q] < p)) { gv = rv[q]; p = ri[q]; }
-      if (tid == 0 && rank == 0 && !(gv > 0.0)) *status = 1;
+      double gv = lane < GJC ? rv[lane] : -1.0;
+      int gp = lane < GJC ? ri[lane] : N;
+#pragma unroll
+      for (int off = GJC / 2; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, gv, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, gp, off);
+        if (ov > gv || (ov == gv && oi < gp)) { gv = ov; gp = oi; }
+      }
+      if (lane == 0) {
+        psh = gp;
+        if (rank == 0 && !(gv > 0.0)) *status = 1;
+      }
     }
+    __syncthreads();
+    const int p = psh;
     const int op = p / R, ok = k / R;
     const double* rowp = cl.map_shared_rank(A, op) + (size_t)(p - op * R) * N;
     const double piv = rowp[k];
