@@ -10,6 +10,9 @@
  *        (grad) mu_T |T|  g_i.g_j d_ab
  *   B_T  -(|T|/4) g_j[b]
  *   C_T  (delta h^2 / mu_T) |T| g_i.g_j                                  reading R1
+ * Per-element coefficients are passed as arrays: emu[e] = mu_T of A and
+ * eimu[e] = the 1/mu_T weight of C (equal to 1/emu on the finest level; the
+ * coarse-level means of reading R15 on coarse levels).
  * with g_i = grad(lambda_i) obtained by inverting the 4x4 vertex matrix.
  * Velocity DoFs on the closure of Dirichlet faces are ignored on input and
  * written as 0 on output.  No stencils, no blocking: a loop over elements.
@@ -101,7 +104,7 @@ static inline int is_dirichlet(int n, const int32_t* faces, int i, int j, int k)
 /* contribution of element (ci,cj,ck,t) to the rows of its local vertices; rows
  * of local vertex m are added only if row_ok[m].  x, y indexed with plane offset. */
 static void element_apply(int n, int form, double delta, const int32_t* faces, const elem_t* e,
-                          double mu, int ci, int cj, int ck, const double* x, double* y,
+                          double mu, double imu, int ci, int cj, int ck, const double* x, double* y,
                           int64_t V, unsigned blocks, int kv0, int kv1) {
   const int64_t N1 = n + 1;
   double xl[16], yl[16];
@@ -125,7 +128,7 @@ static void element_apply(int n, int form, double delta, const int32_t* faces, c
   for (int r = 0; r < 4; ++r) {
     double s = 0.0;
     if (blocks & 4) for (int c = 0; c < 12; ++c) s += e->B[r][c] * xl[c];
-    if (blocks & 8) for (int c = 0; c < 4; ++c) s -= (delta / mu) * e->C[r][c] * xl[12 + c];
+    if (blocks & 8) for (int c = 0; c < 4; ++c) s -= (delta * imu) * e->C[r][c] * xl[12 + c];
     yl[12 + r] = s;
   }
   for (int m = 0; m < 4; ++m) {
@@ -139,8 +142,8 @@ static void element_apply(int n, int form, double delta, const int32_t* faces, c
 /* y rows of vertex planes [kv0, kv1) (all 4 fields), field-major arrays.
  * x holds the full grid (4 x V); y holds the full grid too (rows outside
  * [kv0,kv1) untouched).  Returns 0. */
-int ora_apply_slab(int n, int form, double delta, const int32_t* faces, const uint8_t* cls,
-                   const double* class_mu, const double* x, double* y, int kv0, int kv1,
+int ora_apply_slab(int n, int form, double delta, const int32_t* faces, const double* emu,
+                   const double* eimu, const double* x, double* y, int kv0, int kv1,
                    unsigned blocks) {
   const int64_t N1 = n + 1, V = N1 * N1 * N1;
   elem_t E[6];
@@ -156,7 +159,7 @@ int ora_apply_slab(int n, int form, double delta, const int32_t* faces, const ui
         for (int ci = 0; ci < n; ++ci)
           for (int t = 0; t < 6; ++t) {
             int64_t eid = 6 * (ci + (int64_t)n * (cj + (int64_t)n * ck)) + t;
-            element_apply(n, form, delta, faces, &E[t], class_mu[cls[eid]], ci, cj, ck, x, y, V,
+            element_apply(n, form, delta, faces, &E[t], emu[eid], eimu[eid], ci, cj, ck, x, y, V,
                           blocks, kv0, kv1);
           }
     }
@@ -166,8 +169,8 @@ int ora_apply_slab(int n, int form, double delta, const int32_t* faces, const ui
 
 /* rows (4 fields) of the listed vertices: out[4*s + f].  Loops over the 24
  * elements incident to each vertex and keeps only that vertex's rows. */
-int ora_apply_rows(int n, int form, double delta, const int32_t* faces, const uint8_t* cls,
-                   const double* class_mu, const double* x, const int64_t* verts, int64_t nverts,
+int ora_apply_rows(int n, int form, double delta, const int32_t* faces, const double* emu,
+                   const double* eimu, const double* x, const int64_t* verts, int64_t nverts,
                    double* out) {
   const int64_t N1 = n + 1, V = N1 * N1 * N1;
   elem_t E[6];
@@ -200,7 +203,7 @@ int ora_apply_rows(int n, int form, double delta, const int32_t* faces, const ui
               xl[12 + q] = x[3 * V + vid[q]];
             }
             int64_t eid = 6 * (ci + (int64_t)n * (cj + (int64_t)n * ck)) + t;
-            double mu = class_mu[cls[eid]];
+            double mu = emu[eid], imu = eimu[eid];
             const double (*A)[12] = e->A[form];
             for (int a = 0; a < 3; ++a) {
               int r = a * 4 + m;
@@ -211,7 +214,7 @@ int ora_apply_rows(int n, int form, double delta, const int32_t* faces, const ui
             }
             double sp = 0.0;
             for (int c = 0; c < 12; ++c) sp += e->B[m][c] * xl[c];
-            for (int c = 0; c < 4; ++c) sp -= (delta / mu) * e->C[m][c] * xl[12 + c];
+            for (int c = 0; c < 4; ++c) sp -= (delta * imu) * e->C[m][c] * xl[12 + c];
             acc[3] += sp;
           }
         }
@@ -223,8 +226,8 @@ int ora_apply_rows(int n, int form, double delta, const int32_t* faces, const ui
 }
 
 /* diagonals of A (3 x V, per component) and C (V) by the element loop */
-int ora_diag(int n, int form, double delta, const int32_t* faces, const uint8_t* cls,
-             const double* class_mu, double* dA, double* dC) {
+int ora_diag(int n, int form, double delta, const int32_t* faces, const double* emu,
+             const double* eimu, double* dA, double* dC) {
   const int64_t N1 = n + 1, V = N1 * N1 * N1;
   elem_t E[6];
   build_elements(1.0 / n, E);
@@ -235,11 +238,12 @@ int ora_diag(int n, int form, double delta, const int32_t* faces, const uint8_t*
       for (int ci = 0; ci < n; ++ci)
         for (int t = 0; t < 6; ++t) {
           const elem_t* e = &E[t];
-          double mu = class_mu[cls[6 * (ci + (int64_t)n * (cj + (int64_t)n * ck)) + t]];
+          const int64_t eid = 6 * (ci + (int64_t)n * (cj + (int64_t)n * ck)) + t;
+          double mu = emu[eid], imu = eimu[eid];
           for (int m = 0; m < 4; ++m) {
             int64_t v = (ci + e->off[m][0]) + N1 * ((cj + e->off[m][1]) + N1 * (int64_t)(ck + e->off[m][2]));
             for (int a = 0; a < 3; ++a) dA[a * V + v] += mu * e->A[form][a * 4 + m][a * 4 + m];
-            dC[v] += (delta / mu) * e->C[m][m];
+            dC[v] += (delta * imu) * e->C[m][m];
           }
         }
   (void)faces;

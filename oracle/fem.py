@@ -14,6 +14,8 @@ Divergence  b(v,q) = -(div v, q)
 Stabilisation c(p,q) = sum_T (delta h^2 / mu_T) (grad p, grad q)_T
             (Brezzi-Pitkaranta type; constant and mu-weighting are the
              DESIGN.md reading R1 — the paper does not print the P1-P1 form)
+            On coarse multigrid levels the viscosity of A and the 1/mu weight of C
+            (and of the gauge) are separate per-element arrays (reading R15).
 Saddle system  [[A, B^T], [B, -C]] (u, p) = (f_h, 0)   P:1222-1235.
 
 Vectors are field-major: [u1 (V), u2 (V), u3 (V), p (V)], vertex
@@ -124,11 +126,16 @@ class Problem:
     """One grid level: n, element viscosities, faces, form, delta."""
 
     def __init__(self, n: int, elem_mu: np.ndarray, faces, form: str = "mod",
-                 delta: float = 1.0 / 12.0):
+                 delta: float = 1.0 / 12.0, elem_imu_c: np.ndarray | None = None):
+        """elem_mu: mu_T of the viscous block A per element [k][j][i][t];
+        elem_imu_c: the 1/mu_T weight of C and of the gauge (default 1/elem_mu;
+        coarse levels pass their own, reading R15)."""
         self.n = n
         self.h = 1.0 / n
         self.V = (n + 1) ** 3
         self.elem_mu = np.asarray(elem_mu, dtype=np.float64).reshape(n, n, n, 6)
+        self.elem_imu_c = (1.0 / self.elem_mu if elem_imu_c is None else
+                           np.asarray(elem_imu_c, dtype=np.float64).reshape(n, n, n, 6))
         self.faces = tuple(faces)
         self.form = form
         self.delta = delta
@@ -149,6 +156,7 @@ class Problem:
             em = element_matrices(t, self.h, self.form)
             vid = _element_vertex_ids(n, t)                    # (E,4)
             mu = self.elem_mu[..., t].reshape(-1)              # (E,)
+            imu = self.elem_imu_c[..., t].reshape(-1)          # (E,)
             gidx = np.concatenate([vid + a * V for a in range(3)], axis=1)   # (E,12)
             rowsA.append(np.repeat(gidx, 12, axis=1).reshape(-1))
             colsA.append(np.tile(gidx, (1, 12)).reshape(-1))
@@ -158,11 +166,11 @@ class Problem:
             valsB.append(np.broadcast_to(em["B"].reshape(1, -1), (len(mu), 48)).reshape(-1))
             rowsC.append(np.repeat(vid, 4, axis=1).reshape(-1))
             colsC.append(np.tile(vid, (1, 4)).reshape(-1))
-            valsC.append(((self.delta / mu)[:, None] * em["C"].reshape(1, -1)).reshape(-1))
+            valsC.append(((self.delta * imu)[:, None] * em["C"].reshape(1, -1)).reshape(-1))
             rowsM.append(rowsC[-1])
             colsM.append(colsC[-1])
             valsM.append(np.broadcast_to(em["M"].reshape(1, -1), (len(mu), 16)).reshape(-1))
-            np.add.at(w, vid.reshape(-1), np.repeat(em["vol"] / (4.0 * mu), 4))
+            np.add.at(w, vid.reshape(-1), np.repeat(em["vol"] * imu / 4.0, 4))
         cat = np.concatenate
         self.A = sp.csr_matrix((cat(valsA), (cat(rowsA), cat(colsA))), shape=(3 * V, 3 * V))
         self.B = sp.csr_matrix((cat(valsB), (cat(rowsB), cat(colsB))), shape=(V, 3 * V))

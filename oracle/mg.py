@@ -18,9 +18,15 @@ Written from PAPER.md §5 with assembled scipy matrices:
   on level l (l = 0 finest; reading R13).
 * "Standard restriction and prolongation": P = coarse P1 basis evaluated
   at fine vertices (plain definition of the nodal interpolation), R = P^T.
-* Coarse operators rediscretised per level (h_l = 1/n_l); coarse viscosity class
-  of a coarse tet = majority class of the fine tets it contains (ties -> larger mu,
-  then smaller class id).  Reading R15.
+* Coarse operators rediscretised per level (h_l = 1/n_l) with per-element coarse
+  viscosities (reading R15): for a coarse tet T_c with Bey children
+  T_1..T_8 (the fine tets whose centroids lie in T_c)
+      mu_A(T_c)    = (1/8) sum_q mu_A(T_q)        arithmetic mean  (viscous block A)
+      1/mu_C(T_c)  = (1/8) sum_q 1/mu_C(T_q)      harmonic mean    (weight of C, gauge)
+  The first makes the rediscretised coarse A equal to the Galerkin product
+  P^T A_f P of the nested P1 spaces (R = P^T, "standard" transfers P:1243); the
+  second gives C the Galerkin viscosity weight at the coarse h_l.  A coarse tet's
+  class is the common class of its children, or MIXED.
 * Coarsest level: exact solve ("a direct coarse grid solver ... is not
   problematic") of the free-DoF system; without a traction face the pressure
   constant is fixed by the Lagrange row w^T p = 0 (reading R9/R16).
@@ -84,40 +90,54 @@ def prolongation(nc: int) -> sp.csr_matrix:
     return P
 
 
-def coarse_classes(nf: int, cls_f: np.ndarray, class_mu) -> np.ndarray:
-    """Coarse element classes: majority vote over the 8 fine tets inside each coarse
-    tet (fine tet assigned to the coarse tet containing its centroid)."""
+MIXED = 0xFE   # class of a coarse tet whose children do not share one class
+
+
+def child_parent(nf: int) -> np.ndarray:
+    """For every fine tet (flattened [k][j][i][t]) the flattened index of the coarse
+    tet (grid nf/2) that contains its centroid: the Bey parent."""
     nc = nf // 2
-    class_mu = np.asarray(class_mu, dtype=np.float64)
-    K = len(class_mu)
-    cls_f = np.asarray(cls_f).reshape(nf, nf, nf, 6)
-    counts = np.zeros((nc, nc, nc, 6, K), dtype=np.int64)
     idx = np.arange(nf)
     kk, jj, ii = np.meshgrid(idx, idx, idx, indexing="ij")
+    out = np.empty((nf, nf, nf, 6), dtype=np.int64)
     for t in range(6):
         cen = kuhn_vertices(t).mean(axis=0)
         pts = np.stack([ii.reshape(-1) + cen[0], jj.reshape(-1) + cen[1],
                         kk.reshape(-1) + cen[2]], axis=1) / 2.0
         cube, tc, _ = _locate(pts, nc, strict=True)
-        c = cls_f[..., t].reshape(-1)
-        np.add.at(counts, (cube[:, 2], cube[:, 1], cube[:, 0], tc, c), 1)
-    assert (counts.sum(axis=-1) == 8).all()
-    # majority; ties -> larger mu, then smaller class id
-    order = sorted(range(K), key=lambda q: (-class_mu[q], q))
-    best = np.full(counts.shape[:-1], order[0])
-    bestc = counts[..., order[0]]
-    for q in order[1:]:
-        better = counts[..., q] > bestc
-        best = np.where(better, q, best)
-        bestc = np.where(better, counts[..., q], bestc)
-    return best.astype(np.uint8).reshape(-1)
+        out[..., t] = (6 * (cube[:, 0] + nc * (cube[:, 1] + nc * cube[:, 2])) + tc).reshape(nf, nf, nf)
+    out = out.reshape(-1)
+    assert (np.bincount(out, minlength=6 * nc ** 3) == 8).all()
+    return out
+
+
+def coarse_viscosity(nf: int, mu_a: np.ndarray, imu_c: np.ndarray):
+    """Coarse per-element (mu_A, 1/mu_C): means over the 8 Bey children (reading R15)."""
+    par = child_parent(nf)
+    E = 6 * (nf // 2) ** 3
+    mu_c = np.bincount(par, weights=np.asarray(mu_a, dtype=np.float64).reshape(-1), minlength=E) / 8.0
+    imu_cc = np.bincount(par, weights=np.asarray(imu_c, dtype=np.float64).reshape(-1), minlength=E) / 8.0
+    return mu_c, imu_cc
+
+
+def coarse_classes(nf: int, cls_f: np.ndarray) -> np.ndarray:
+    """Coarse class: the class shared by all 8 Bey children, else MIXED."""
+    par = child_parent(nf)
+    E = 6 * (nf // 2) ** 3
+    c = np.asarray(cls_f, dtype=np.int64).reshape(-1)
+    lo = np.full(E, 1 << 20)
+    hi = np.full(E, -1)
+    np.minimum.at(lo, par, c)
+    np.maximum.at(hi, par, c)
+    return np.where(lo == hi, lo, MIXED).astype(np.uint8)
 
 
 class Level:
-    def __init__(self, n, cls, class_mu, faces, form, delta):
+    def __init__(self, n, cls, mu_a, imu_c, faces, form, delta):
         self.n = n
         self.cls = np.asarray(cls, dtype=np.uint8)
-        self.prob = Problem(n, np.asarray(class_mu)[self.cls], faces, form, delta)
+        self.mu_a, self.imu_c = mu_a, imu_c
+        self.prob = Problem(n, mu_a, faces, form, delta, elem_imu_c=imu_c)
         i, j, k = vertex_coords(n)
         self.parity = (i + j + k)
         V = self.prob.V
@@ -132,14 +152,17 @@ class Hierarchy:
         self.levels = []
         self.P = []
         c = np.asarray(cls, dtype=np.uint8)
+        mu_a = np.asarray(class_mu, dtype=np.float64)[c]
+        imu_c = 1.0 / mu_a
         m = n
         while True:
-            self.levels.append(Level(m, c, class_mu, faces, form, delta))
+            self.levels.append(Level(m, c, mu_a, imu_c, faces, form, delta))
             if m <= n_coarse:
                 break
             assert m % 2 == 0
             self.P.append(prolongation(m // 2))
-            c = coarse_classes(m, c, class_mu)
+            mu_a, imu_c = coarse_viscosity(m, mu_a, imu_c)
+            c = coarse_classes(m, c)
             m //= 2
         self.nu_pre, self.nu_post, self.nu_inc = nu_pre, nu_post, nu_inc
         self.omega = omega
@@ -223,3 +246,36 @@ class Hierarchy:
             if hist[-1] <= rtol:
                 break
         return top.gauge(x), hist
+
+    def solve_krylov(self, b, rtol=1e-12, restart=30, maxiter=400):
+        """GMRES(restart) (scipy, a library primitive) on the free-DoF system K_FF x = b_F,
+        preconditioned by one V_var cycle from a zero guess: the outer iteration used
+        when the plain V-cycle iteration does not converge (unresolved high-contrast
+        inclusions).  Returns the gauged solution and the true relative
+        residual."""
+        import scipy.sparse.linalg as spla
+        top = self.levels[0].prob
+        free = np.flatnonzero(top.free)
+        n4 = 4 * top.V
+        if hasattr(top, "K"):
+            Kf = top.K_free()
+            matvec = Kf.__matmul__
+        else:
+            def matvec(v):
+                x = np.zeros(n4)
+                x[free] = v
+                return top.apply(x)[free]
+
+        def prec(r):
+            full = np.zeros(n4)
+            full[free] = r
+            return self.vcycle(full, np.zeros(n4))[free]
+
+        N = len(free)
+        Aop = spla.LinearOperator((N, N), matvec=matvec)
+        M = spla.LinearOperator((N, N), matvec=prec)
+        xf, info = spla.gmres(Aop, b[free], M=M, rtol=rtol, atol=0.0, restart=restart, maxiter=maxiter)
+        x = np.zeros(n4)
+        x[free] = xf
+        rel = np.linalg.norm(b - top.apply(x)) / np.linalg.norm(b)
+        return top.gauge(x), rel

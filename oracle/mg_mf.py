@@ -28,11 +28,11 @@ class _Op:
 class MFProblem:
     """Matrix-free level: products by the C element loop (blocks A, B^T, B, C)."""
 
-    def __init__(self, n, cls, class_mu, faces, form="mod", delta=1.0 / 12.0):
+    def __init__(self, n, mu_a, imu_c, faces, form="mod", delta=1.0 / 12.0):
         self.n, self.V = n, (n + 1) ** 3
         self.h = 1.0 / n
-        self.cls = np.ascontiguousarray(cls, dtype=np.uint8)
-        self.class_mu = np.asarray(class_mu, dtype=np.float64)
+        self.mu_a = np.ascontiguousarray(mu_a, dtype=np.float64)
+        self.imu_c = np.ascontiguousarray(imu_c, dtype=np.float64)
         self.faces, self.form, self.delta = tuple(faces), form, delta
         self.dir_v = dirichlet_vertex_mask(n, self.faces)
         self.free = np.concatenate([~self.dir_v] * 3 + [np.ones(self.V, dtype=bool)])
@@ -40,7 +40,8 @@ class MFProblem:
         V = self.V
 
         def ap(vec, blocks):
-            return capi.apply_slab(n, form, delta, self.faces, self.cls, self.class_mu, vec, blocks=blocks)
+            return capi.apply_slab(n, form, delta, self.faces, None, None, vec, blocks=blocks,
+                                   mu_a=self.mu_a, imu_c=self.imu_c)
 
         def A(u):
             return ap(np.concatenate([u, np.zeros(V)]), 1)[:3 * V]
@@ -58,14 +59,14 @@ class MFProblem:
         self.B = _Op(B, _Op(BT))
         self.C = _Op(C)
         self._ap = ap
-        dA, dC = capi.diagonals(n, form, delta, self.faces, self.cls, self.class_mu)
+        dA, dC = capi.diagonals(n, form, delta, self.faces, None, None, mu_a=self.mu_a, imu_c=self.imu_c)
         self.diagA, self.diagC = dA, dC
         # gauge weights w_j = sum_T |T| / (4 mu_T)
         w = np.zeros(V)
-        mu = self.class_mu[self.cls].reshape(n, n, n, 6)
+        imu = self.imu_c.reshape(n, n, n, 6)
         for t in range(6):
             vid = fem._element_vertex_ids(n, t)
-            np.add.at(w, vid.reshape(-1), np.repeat((self.h ** 3 / 6) / (4.0 * mu[..., t].reshape(-1)), 4))
+            np.add.at(w, vid.reshape(-1), np.repeat((self.h ** 3 / 6) * imu[..., t].reshape(-1) / 4.0, 4))
         self.gauge_w = w
 
     def apply(self, x):
@@ -75,15 +76,16 @@ class MFProblem:
 
 
 class MFLevel:
-    def __init__(self, n, cls, class_mu, faces, form, delta):
+    def __init__(self, n, cls, mu_a, imu_c, faces, form, delta):
         self.n = n
         self.cls = np.asarray(cls, dtype=np.uint8)
+        self.mu_a, self.imu_c = mu_a, imu_c
         if n <= 16:
-            self.prob = fem.Problem(n, np.asarray(class_mu)[self.cls], faces, form, delta)
+            self.prob = fem.Problem(n, mu_a, faces, form, delta, elem_imu_c=imu_c)
             self.diagA = self.prob.A.diagonal()
             self.diagC = self.prob.C.diagonal()
         else:
-            self.prob = MFProblem(n, cls, class_mu, faces, form, delta)
+            self.prob = MFProblem(n, mu_a, imu_c, faces, form, delta)
             self.diagA, self.diagC = self.prob.diagA, self.prob.diagC
         i, j, k = mg.vertex_coords(n)
         self.parity = i + j + k
@@ -95,13 +97,16 @@ class MFHierarchy(mg.Hierarchy):
                  n_coarse=4, nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2):
         self.levels, self.P = [], []
         c = np.asarray(cls, dtype=np.uint8)
+        mu_a = np.asarray(class_mu, dtype=np.float64)[c]
+        imu_c = 1.0 / mu_a
         m = n
         while True:
-            self.levels.append(MFLevel(m, c, class_mu, faces, form, delta))
+            self.levels.append(MFLevel(m, c, mu_a, imu_c, faces, form, delta))
             if m <= n_coarse:
                 break
             self.P.append(mg.prolongation(m // 2))
-            c = mg.coarse_classes(m, c, class_mu)
+            mu_a, imu_c = mg.coarse_viscosity(m, mu_a, imu_c)
+            c = mg.coarse_classes(m, c)
             m //= 2
         self.nu_pre, self.nu_post, self.nu_inc = nu_pre, nu_post, nu_inc
         self.omega = omega

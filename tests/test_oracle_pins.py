@@ -264,37 +264,158 @@ def test_prolongation_reproduces_linears():
 
 
 def test_coarse_classes_of_resolved_interface_equal_rediscretisation():
-    for name in ("cfg1", "cfg5"):
-        cf = synth.get_config(name, n=16)
-        cc = synth.get_config(name, n=8)
-        if name == "cfg5":       # lid z>0.9 is not resolved at n=8/16: use the majority rule check only
-            continue
-        cls_f, _ = synth.element_classes(cf)
-        cls_c, _ = synth.element_classes(cc)
-        got = mg.coarse_classes(16, cls_f, cf.class_mu)
-        np.testing.assert_array_equal(got, cls_c)
+    # a resolved interface (cfg1 plane x = 1/2) gives pure coarse classes that equal
+    # the direct classification of the coarse grid (no MIXED tet)
+    cf = synth.get_config("cfg1", n=16)
+    cc = synth.get_config("cfg1", n=8)
+    cls_f, _ = synth.element_classes(cf)
+    cls_c, _ = synth.element_classes(cc)
+    got = mg.coarse_classes(16, cls_f)
+    np.testing.assert_array_equal(got, cls_c)
+    mu_a, imu_c = mg.coarse_viscosity(16, np.asarray(cf.class_mu)[cls_f], 1.0 / np.asarray(cf.class_mu)[cls_f])
+    np.testing.assert_allclose(mu_a, np.asarray(cf.class_mu)[cls_c], rtol=1e-15)
+    np.testing.assert_allclose(imu_c, 1.0 / np.asarray(cf.class_mu)[cls_c], rtol=1e-15)
 
 
-def test_coarse_classes_majority_brute_force():
-    # tiny brute force: every coarse tet gets the class held by most of its 8 children
+def _bey_children_brute(nf, K, J, I, T):
+    """Fine tets whose centroid lies strictly inside coarse tet (K,J,I,T)."""
+    verts = (fem.kuhn_vertices(T) + np.array([I, J, K])) * 2.0
+    Xc = np.hstack([np.ones((4, 1)), verts])
+    out = []
+    for k, j, i, t in itertools.product(range(nf), range(nf), range(nf), range(6)):
+        cen = (fem.kuhn_vertices(t) + np.array([i, j, k])).mean(axis=0)
+        lam = np.linalg.solve(Xc.T, np.concatenate([[1.0], cen]))
+        if (lam > 1e-12).all():
+            out.append(((k * nf + j) * nf + i) * 6 + t)
+    return out
+
+
+def test_coarse_viscosity_and_class_brute_force():
+    # reading R15 by brute force: every coarse tet has exactly 8 Bey children; mu_A is
+    # their arithmetic mean, 1/mu_C the mean of their 1/mu, the class is shared or MIXED
     rng = np.random.default_rng(5)
     nf = 4
     cls = rng.integers(0, 3, size=6 * nf ** 3).astype(np.uint8)
-    mu = (1.0, 7.0, 3.0)
-    got = mg.coarse_classes(nf, cls, mu).reshape(2, 2, 2, 6)
-    c4 = cls.reshape(nf, nf, nf, 6)
+    cls[:6 * nf * nf] = 1                  # a layer of pure coarse tets too
+    mu = np.array([1.0, 7.0, 3.0])
+    mu_a, imu_c = mg.coarse_viscosity(nf, mu[cls], 1.0 / mu[cls])
+    cc = mg.coarse_classes(nf, cls)
+    seen_mixed = seen_pure = False
     for K, J, I, T in itertools.product(range(2), range(2), range(2), range(6)):
-        verts = (fem.kuhn_vertices(T) + np.array([I, J, K])) * 2.0
-        Xc = np.hstack([np.ones((4, 1)), verts])
-        votes = np.zeros(3, int)
-        for k, j, i, t in itertools.product(range(nf), range(nf), range(nf), range(6)):
-            cen = (fem.kuhn_vertices(t) + np.array([i, j, k])).mean(axis=0)
-            lam = np.linalg.solve(Xc.T, np.concatenate([[1.0], cen]))
-            if (lam > 1e-12).all():
-                votes[c4[k, j, i, t]] += 1
-        assert votes.sum() == 8
-        best = max(range(3), key=lambda q: (votes[q], mu[q], -q))
-        assert got[K, J, I, T] == best
+        ch = _bey_children_brute(nf, K, J, I, T)
+        assert len(ch) == 8
+        e = ((K * 2 + J) * 2 + I) * 6 + T
+        assert mu_a[e] == pytest.approx(np.mean(mu[cls[ch]]), rel=1e-15)
+        assert imu_c[e] == pytest.approx(np.mean(1.0 / mu[cls[ch]]), rel=1e-15)
+        if len(set(cls[ch])) == 1:
+            assert cc[e] == cls[ch[0]]
+            seen_pure = True
+        else:
+            assert cc[e] == mg.MIXED
+            seen_mixed = True
+    assert seen_mixed and seen_pure
+
+
+@pytest.mark.parametrize("form", ["mod", "sym", "grad"])
+def test_coarse_operators_are_galerkin_products(form):
+    # R15 pinned against the Galerkin products of the nested P1 spaces (P:573-574,
+    # R = P^T, P:1243): with mu_A the arithmetic mean of the children, the coarse
+    # A equals P^T A_f P; B_c = P^T B_f P exactly; with 1/mu_C the mean of 1/mu the
+    # coarse C equals 4 P^T C_f P (C carries h_l^2, R1, and h_c = 2 h_f).
+    nf, nc = 8, 4
+    rng = np.random.default_rng(11)
+    mu_f = np.array([1.0, 1e3, 30.0])[rng.integers(0, 3, size=6 * nf ** 3)]
+    faces = synth.TOP_TRACTION
+    pf = fem.Problem(nf, mu_f, faces, form)
+    mu_a, imu_c = mg.coarse_viscosity(nf, mu_f, 1.0 / mu_f)
+    pc = fem.Problem(nc, mu_a, faces, form, elem_imu_c=imu_c)
+    P = mg.prolongation(nc)
+    P3 = sp.block_diag([P] * 3).tocsr()
+    fu = sp.diags(pf.free[:3 * pf.V].astype(float))
+    cu = pc.free[:3 * pc.V]
+    Ag = (P3.T @ fu @ pf.A @ fu @ P3).toarray()[np.ix_(cu, cu)]
+    Ac = pc.A.toarray()[np.ix_(cu, cu)]
+    assert np.abs(Ag - Ac).max() <= 1e-12 * np.abs(Ac).max()
+    Bg = (P.T @ pf.B @ fu @ P3).toarray()[:, cu]
+    np.testing.assert_allclose(Bg, pc.B.toarray()[:, cu], atol=1e-14 * np.abs(Bg).max())
+    Cg = 4.0 * (P.T @ pf.C @ P).toarray()
+    np.testing.assert_allclose(Cg, pc.C.toarray(), atol=1e-12 * np.abs(Cg).max())
+    # the gauge weights keep int_Omega 1/mu (the coarse weight of a tet is |T_c| times
+    # the mean of 1/mu over its children)
+    assert pc.gauge_w.sum() == pytest.approx(pf.gauge_w.sum(), rel=1e-13)
+
+
+# -- P:136: Q = {q : int mu^-1 q = 0}; gauge weights w_j = int phi_j / mu -------------
+def test_gauge_weights_closed_forms():
+    n = 8
+    pr, cls = _cfg1_problem(n, "mod", mu=(10.0, 1.0))
+    # sum_j w_j = int_Omega 1/mu = |Omega_1|/mu_1 + |Omega_2|/mu_2 (plane x = 1/2)
+    assert pr.gauge_w.sum() == pytest.approx(0.5 / 10.0 + 0.5 / 1.0, rel=1e-13)
+    # an isoviscous interior vertex: int phi_j = h^3 (mu = 10 left, 1 right)
+    i, j, k = mg.vertex_coords(n)
+    inner = (i > 0) & (j > 0) & (k > 0) & (i < n) & (j < n) & (k < n)
+    left, right = inner & (2 * i < n), inner & (2 * i > n)
+    np.testing.assert_allclose(pr.gauge_w[left], (1 / n) ** 3 / 10.0, rtol=1e-13)
+    np.testing.assert_allclose(pr.gauge_w[right], (1 / n) ** 3 / 1.0, rtol=1e-13)
+    # a constant pressure is gauged to 0; a gauged field has zero weighted mean
+    x = np.zeros(4 * pr.V)
+    x[3 * pr.V:] = 3.7
+    assert np.abs(pr.gauge(x)[3 * pr.V:]).max() < 1e-13
+    rng = np.random.default_rng(2)
+    x[3 * pr.V:] = rng.standard_normal(pr.V)
+    assert abs(pr.gauge_w @ pr.gauge(x)[3 * pr.V:]) < 1e-14
+
+
+# -- consistent mass (load_nodal) against the App. A.2 closed-form stencil -----------
+def test_load_nodal_matches_mass_stencil():
+    n = 6
+    pr, _ = _cfg1_problem(n, "mod")
+    h = 1.0 / n
+    N1 = n + 1
+    rng = np.random.default_rng(4)
+    f = rng.standard_normal((3, pr.V))
+    b = pr.load_nodal(f).reshape(4, pr.V)
+    # interior row of M: h^3 [2/5 centre; 1/20 at +-e_s and +-(1,1,1); 1/30 at
+    # +-(1,1,0), +-(1,0,1), +-(0,1,1)]  (SURVEY App. A.2)
+    sten = {(0, 0, 0): 2 / 5}
+    for d in [(1, 0, 0), (0, 1, 0), (0, 0, 1), (1, 1, 1)]:
+        sten[d] = sten[tuple(-c for c in d)] = 1 / 20
+    for d in [(1, 1, 0), (1, 0, 1), (0, 1, 1)]:
+        sten[d] = sten[tuple(-c for c in d)] = 1 / 30
+    assert sum(sten.values()) == pytest.approx(1.0)
+    for (i, j, k) in [(1, 1, 1), (3, 2, 4), (5, 5, 5), (2, 4, 1)]:
+        v = i + N1 * (j + N1 * k)
+        for a in range(3):
+            want = h ** 3 * sum(w * f[a, (i + d[0]) + N1 * ((j + d[1]) + N1 * (k + d[2]))]
+                                for d, w in sten.items())
+            assert b[a, v] == pytest.approx(want, rel=1e-12)
+    assert np.abs(b[3]).max() == 0.0                       # b_p = 0 (P:1230-1233)
+    dmask = synth.dirichlet_vertex_mask(n, synth.ALL_DIRICHLET)
+    assert np.abs(b[:3, dmask]).max() == 0.0
+
+
+def test_load_element_brute_force_and_total():
+    # element-constant f: b_{i,a} = sum_{T ni i} f_{T,a} |T| / 4 (R10).  Brute force
+    # on one tet, and sum_i b_{i,a} = int f_a when no vertex is constrained.
+    n = 3
+    faces = (synth.TRACTION,) * 6                           # no constrained velocity row
+    pr = fem.Problem(n, np.ones(6 * n ** 3), faces, "mod")
+    rng = np.random.default_rng(6)
+    E = 6 * n ** 3
+    fe = rng.standard_normal((E, 3))
+    b = pr.load_element(fe).reshape(4, pr.V)
+    vol = (1 / n) ** 3 / 6
+    np.testing.assert_allclose(b[:3].sum(axis=1), fe.sum(axis=0) * vol, rtol=1e-12)
+    one = np.zeros((E, 3))
+    e = 6 * (1 + n * (2 + n * 0)) + 4                         # cube (1,2,0), tet 4
+    one[e] = (1.0, -2.0, 0.5)
+    b1 = pr.load_element(one).reshape(4, pr.V)
+    verts = fem.kuhn_vertices(4).astype(int) + np.array([1, 2, 0])
+    ids = [vx + (n + 1) * (vy + (n + 1) * vz) for vx, vy, vz in verts]
+    want = np.zeros((3, pr.V))
+    for v in ids:
+        want[:, v] = np.array([1.0, -2.0, 0.5]) * vol / 4
+    np.testing.assert_allclose(b1[:3], want, atol=1e-17)
 
 
 # -- smoother: Jacobi-within-colour == Gauss-Seidel for rows without same-colour coupling
@@ -327,6 +448,45 @@ def test_colour_pass_equals_sequential_gauss_seidel_on_7pt_rows():
     hx.omega = 0.0
     out = hx.uzawa(lev, x, b)
     np.testing.assert_allclose(out[:3 * V], u, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("faces", [synth.ALL_DIRICHLET, synth.TOP_TRACTION])
+def test_pressure_sweep_equals_sequential_forward_gauss_seidel(faces):
+    # S^ of P:1243 ("forward variant of the Gauss-Seidel method applied to ... C,
+    # omega = 0.3"), reading R11: delta = one forward Gauss-Seidel sweep on
+    # C delta = r_p from 0 in red-black order, p += omega delta.  Checked against a
+    # row-by-row sequential sweep written here; a Jacobi sweep would fail it.
+    n = 4
+    cfg = synth.get_config("cfg1", n=n)
+    cls, _ = synth.element_classes(cfg)
+    h = mg.Hierarchy(n, cls, (10.0, 1.0), faces, n_coarse=4)
+    lev = h.levels[0]
+    pr = lev.prob
+    V = pr.V
+    rng = np.random.default_rng(8)
+    x = np.where(pr.free, rng.standard_normal(4 * V), 0.0)
+    b = np.where(pr.free, rng.standard_normal(4 * V), 0.0)
+    out = h.uzawa(lev, x, b)
+    u1 = out[:3 * V]                          # velocity half: pinned by the 7-pt test above
+    rp = pr.B @ u1 - pr.C @ x[3 * V:] - b[3 * V:]
+    C = pr.C.tocsr()
+    par = lev.parity % 2
+    # C couples only vertices of different parity (7-point), so red-black = GS
+    Cc = C.tocoo()
+    off = (Cc.row != Cc.col) & (np.abs(Cc.data) > 1e-14 * np.abs(Cc.data).max())
+    assert (par[Cc.row[off]] != par[Cc.col[off]]).all()
+    d = np.zeros(V)
+    for colour in (0, 1):
+        for r in [v for v in range(V) if par[v] == colour]:
+            s_ = rp[r]
+            for idx in range(C.indptr[r], C.indptr[r + 1]):
+                if C.indices[idx] != r:
+                    s_ -= C.data[idx] * d[C.indices[idx]]
+            d[r] = s_ / C[r, r]
+    want = x[3 * V:] + 0.3 * d
+    np.testing.assert_allclose(out[3 * V:], want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
+    jac = x[3 * V:] + 0.3 * rp / C.diagonal()
+    assert np.abs(jac - want).max() > 1e-3 * np.abs(want).max()
 
 
 def test_exact_solution_is_smoother_and_vcycle_fixed_point():
@@ -367,6 +527,24 @@ def test_multigrid_reaches_direct_solution(cfgname, form):
     assert hist[-1] <= 1e-12
     rho = (hist[-1] / hist[3]) ** (1 / (len(hist) - 4))
     assert rho < 0.6
+    for fld in range(4):
+        s = slice(fld * pr.V, (fld + 1) * pr.V)
+        assert np.linalg.norm(x[s] - xd[s]) <= 1e-8 * np.linalg.norm(xd[s])
+
+
+@pytest.mark.parametrize("cfgname", ["cfg3", "cfg5"])
+def test_krylov_multigrid_reaches_direct_solution_high_contrast(cfgname):
+    # unresolved 1e3-1e4 inclusions (BASELINE cfg3, cfg5): GMRES preconditioned by the
+    # V_var cycle with the R15 coarse viscosities reaches the unique discrete solution
+    n = 16
+    cfg = synth.get_config(cfgname, n=n)
+    cls, fcls = synth.element_classes(cfg)
+    h = mg.Hierarchy(n, cls, cfg.class_mu, cfg.faces)
+    pr = h.levels[0].prob
+    b = pr.load_element(fem.element_force(n, fcls, cfg.force_table))
+    xd = pr.gauge(pr.solve_direct(b))
+    x, rel = h.solve_krylov(b, rtol=1e-11)
+    assert rel <= 1e-10
     for fld in range(4):
         s = slice(fld * pr.V, (fld + 1) * pr.V)
         assert np.linalg.norm(x[s] - xd[s]) <= 1e-8 * np.linalg.norm(xd[s])
