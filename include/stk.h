@@ -47,6 +47,8 @@ extern "C" {
 #endif
 
 typedef struct stk_ctx stk_ctx;
+/* a group of nranks contexts of ONE process on ONE device (loopback exchanger) */
+typedef struct stk_loopback stk_loopback;
 
 typedef enum {
   STK_OK = 0,
@@ -109,23 +111,40 @@ typedef struct {
  * (e.g. with torch.distributed), pass to stk_create on every rank. */
 stk_status stk_nccl_unique_id(uint8_t id[128]);
 
-/* Create a context on the current CUDA device.  Checks n (power of 2,
- * n/nranks divisible by 2 on every distributed level).  id may be NULL when
- * nranks == 1. */
+/* Create a context on the current CUDA device (n^3 cubes x 6 tets; the
+ * V_var hierarchy of P:1236 with levels n, n/2, ..., n_coarse).  Checks n (power
+ * of 2, n/nranks divisible by 2 on every distributed level).  id may be NULL when
+ * nranks == 1.  *out is set (to a context holding the error message) even on
+ * failure; destroy it with stk_destroy. */
 stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out);
+
+/* Loopback exchanger: the nranks contexts of one process share one
+ * device and ONE stream (cfg.stream must be equal, else STK_EINVAL); each context is
+ * driven by its own host thread, and every collective (halo planes, allreduce,
+ * coarse agglomeration) is a host rendezvous of the nranks threads followed by one
+ * cudaMemcpyAsync per plane / range.  Same results as nranks GPUs over NCCL (the
+ * apply and V-cycle bitwise equal to nranks = 1).  The group outlives its contexts. */
+stk_status stk_loopback_create(int32_t nranks, stk_loopback** out);
+stk_status stk_create_loopback(const stk_config* cfg, stk_loopback* group, stk_ctx** out);
+stk_status stk_loopback_destroy(stk_loopback* group);
 
 /* Element viscosity partition.  elem_class: host uint8 array of this
  * rank's cube layers cz in [z0_cubes, z1_cubes) (see stk_cube_range), layout
  * [cz][cj][ci][t], t = Kuhn permutation index; class_mu: nclass
- * (<= 255) viscosities > 0.  Both copied. */
+ * (<= 254; ids 0xFE/0xFF are reserved) viscosities > 0.  Both copied.
+ * STK_EINVAL if an element class is >= nclass or a viscosity is not > 0. */
 stk_status stk_set_viscosity(stk_ctx* ctx, const uint8_t* elem_class, const double* class_mu,
                              int32_t nclass);
 /* cube layers [*z0, *z1) this rank must pass to stk_set_viscosity */
 stk_status stk_cube_range(const stk_ctx* ctx, int32_t* z0, int32_t* z1);
 
-/* Assemble all levels: coarse viscosity classes (majority of the 8 Bey children),
- * per-vertex classification (regular class k / interface-or-boundary row),
- * constant subdomain stencils per class, and the coarsest-level inverse. */
+/* Assemble all levels: coarse element coefficients
+ * (DESIGN R15: per coarse tet the arithmetic mean of its 8 Bey children's mu for A
+ * -- the coarse A is then the Galerkin product P^T A P -- and the mean of 1/mu for
+ * C; the class is the children's common class or MIXED), per-vertex classification
+ * (regular row of class k: isoviscous star; else an interface / boundary row with
+ * an explicit stencil), constant subdomain stencils per class, and the
+ * coarsest-level inverse (P:1245 direct coarse solve). */
 stk_status stk_assemble(stk_ctx* ctx);
 
 stk_status stk_layout(const stk_ctx* ctx, int32_t level, stk_layout_t* out);
@@ -190,6 +209,15 @@ int32_t stk_row_level(const stk_ctx* ctx);
 stk_status stk_set_fuse_n(stk_ctx* ctx, int32_t fuse_n);
 /* First fused level, or -1 when the fused V-cycle is not used. */
 int32_t stk_fused_level(const stk_ctx* ctx);
+/* Diagnostics for integer parity: the element classes (0xFE = MIXED) of the stored
+ * cube layers of a level ([cz][cj][ci][t], cz0..cz1 as stk_partition reports) and,
+ * if emu_host != NULL, the per-tet (mu_A, 1/mu_C) pairs (2 doubles per tet; zeros on
+ * level 0, whose coefficients are the class table); and the per-vertex row codes of
+ * the owned vertices (canonical layout x fastest): 0..0x3F regular row of that class,
+ * 0x40|k isoviscous traction-face row, 0xFF interface / boundary row (explicit
+ * stencil).  Synchronous. */
+stk_status stk_export_classes(stk_ctx* ctx, int32_t level, uint8_t* cls_host, double* emu_host);
+stk_status stk_export_codes(stk_ctx* ctx, int32_t level, uint8_t* code_host);
 /* Number of kernels this context launched so far (evidence counter). */
 int64_t stk_launch_count(const stk_ctx* ctx);
 

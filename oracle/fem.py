@@ -247,6 +247,25 @@ class Problem:
         return x
 
 
+def load_nodal_elementwise(n: int, faces, f: np.ndarray) -> np.ndarray:
+    """b_u = (M (x) I3) f by the element loop (consistent P1 mass |T|/20 (1 + d_ij) per
+    tet, no assembled matrix: for the matrix-free oracle levels); b_p = 0; zero at
+    Dirichlet rows.  Equals Problem.load_nodal (pinned by the mass-stencil test)."""
+    V = (n + 1) ** 3
+    f = np.asarray(f, dtype=np.float64).reshape(3, V)
+    vol = (1.0 / n) ** 3 / 6.0
+    b = np.zeros((3, V))
+    for t in range(6):
+        vid = _element_vertex_ids(n, t)                    # (E, 4)
+        for a in range(3):
+            fl = f[a][vid]                                 # (E, 4)
+            loc = (vol / 20.0) * (fl.sum(axis=1, keepdims=True) + fl)
+            b[a] += np.bincount(vid.reshape(-1), weights=loc.reshape(-1), minlength=V)
+    dv = dirichlet_vertex_mask(n, faces)
+    b[:, dv] = 0.0
+    return np.concatenate([b.reshape(-1), np.zeros(V)])
+
+
 def problem_from_classes(n, mu_cls, class_mu, faces, form="mod", delta=1.0 / 12.0):
     elem_mu = np.asarray(class_mu, dtype=np.float64)[np.asarray(mu_cls)]
     return Problem(n, elem_mu, faces, form, delta)

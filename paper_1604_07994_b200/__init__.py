@@ -60,6 +60,11 @@ _sigs = {
     "stk_nccl_unique_id": [_P],
     "stk_partition": [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P],
     "stk_create": [ctypes.POINTER(stk_config), _P, ctypes.POINTER(_P)],
+    "stk_loopback_create": [ctypes.c_int32, ctypes.POINTER(_P)],
+    "stk_create_loopback": [ctypes.POINTER(stk_config), _P, ctypes.POINTER(_P)],
+    "stk_loopback_destroy": [_P],
+    "stk_export_classes": [_P, ctypes.c_int32, _P, _P],
+    "stk_export_codes": [_P, ctypes.c_int32, _P],
     "stk_set_viscosity": [_P, _P, _P, ctypes.c_int32],
     "stk_cube_range": [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
     "stk_assemble": [_P],
@@ -132,6 +137,23 @@ def partition(n, nranks, rank, n_coarse=4):
     return [dict(zip(keys, out[8 * l:8 * l + 8])) for l in range(nlev.value)]
 
 
+class LoopbackGroup:
+    """nranks contexts of one process on one device (stk_loopback_create): run each
+    rank's calls in its own thread (ctypes releases the GIL during library calls)."""
+
+    def __init__(self, nranks):
+        h = _P()
+        s = _lib.stk_loopback_create(nranks, ctypes.byref(h))
+        if s != STK_OK:
+            raise StkError("stk_loopback_create", s, "")
+        self.h, self.nranks = h, nranks
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.stk_loopback_destroy(self.h)
+            self.h = None
+
+
 def nccl_unique_id() -> bytes:
     buf = (ctypes.c_uint8 * 128)()
     s = _lib.stk_nccl_unique_id(buf)
@@ -145,7 +167,7 @@ class StokesContext:
 
     def __init__(self, n, form="mod", faces=(0,) * 6, delta=1.0 / 12.0, n_coarse=4,
                  nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2, krylov=0, rank=0, nranks=1,
-                 stream=None, nccl_id: bytes | None = None):
+                 stream=None, nccl_id: bytes | None = None, loopback: LoopbackGroup | None = None):
         import torch
         self.torch = torch
         cfg = stk_config()
@@ -165,7 +187,10 @@ class StokesContext:
         idbuf = None
         if nccl_id is not None:
             idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
-        s = _lib.stk_create(ctypes.byref(cfg), idbuf, ctypes.byref(h))
+        if loopback is not None:
+            s = _lib.stk_create_loopback(ctypes.byref(cfg), loopback.h, ctypes.byref(h))
+        else:
+            s = _lib.stk_create(ctypes.byref(cfg), idbuf, ctypes.byref(h))
         self.h = h
         if s != STK_OK:
             msg = _lib.stk_last_error(h).decode() if h.value else ""
@@ -206,6 +231,25 @@ class StokesContext:
         a, b = ctypes.c_int32(), ctypes.c_int32()
         self._chk("stk_cube_range", _lib.stk_cube_range(self.h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
+
+    def partition(self):
+        return partition(self.n, self.cfg.nranks, self.cfg.rank, self.cfg.n_coarse)
+
+    def export_classes(self, level=0):
+        """(classes uint8 [stored cube layers][n][n][6], emu (.., 2) float64) of a level."""
+        p = self.partition()[level]
+        m = p["n"]
+        cnt = (p["cz1"] - p["cz0"]) * m * m * 6
+        cls = np.empty(cnt, dtype=np.uint8)
+        emu = np.empty((cnt, 2), dtype=np.float64)
+        self._chk("stk_export_classes", _lib.stk_export_classes(self.h, level, _ptr(cls), _ptr(emu)))
+        return cls, emu
+
+    def export_codes(self, level=0):
+        lay = self.layout(level)
+        out = np.empty(lay.n_vertices, dtype=np.uint8)
+        self._chk("stk_export_codes", _lib.stk_export_codes(self.h, level, _ptr(out)))
+        return out
 
     def new_vector(self, level=0):
         return self.torch.zeros(self.layout(level).vec_len, dtype=self.torch.float64, device="cuda")

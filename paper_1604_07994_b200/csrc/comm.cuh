@@ -1,10 +1,25 @@
 // Z-slab communication: one vertex plane per neighbour per
-// exchange (ncclSend/ncclRecv in a group on the solver stream), an fp64
-// allreduce for the norms / gauge sums (once per cycle), and the agglomeration
-// of the coarsest levels onto every rank (each rank broadcasts its planes).
-// With one rank every call is a no-op.
+// exchange, an fp64 allreduce for the norms / gauge sums (once per cycle), the
+// agglomeration of the coarsest levels onto every rank, and the one cube layer of
+// coarse element data a rank takes from the rank below.  With one rank every call
+// is a no-op.
+//
+// Two backends behind the same calls:
+//  * NCCL: one process (rank) per GPU; ncclSend/ncclRecv/ncclBroadcast/ncclAllReduce
+//    on the solver stream (the production multi-GPU path over NVLink / NVSwitch).
+//  * loopback: P contexts of one process on ONE device, each driven by its own host
+//    thread and all on the same CUDA stream (stk_loopback_create).  A collective is a
+//    host rendezvous of the P threads: every rank publishes its buffer, then copies
+//    from its peers' buffers with one cudaMemcpyAsync per plane or range, then a
+//    second rendezvous keeps any rank from enqueueing work that overwrites a buffer
+//    before every peer's copy out of it is enqueued (stream order does the rest).  No
+//    kernel waits on another.  It makes the P-rank code path (partition, halos, split
+//    levels, agglomeration) testable on one GPU: results must equal P = 1 (T4).
 #pragma once
+#include <condition_variable>
 #include <cstdint>
+#include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -44,49 +59,71 @@ __global__ void k_restrict_part(DGrid gf, DGrid gc, int K0, int K1, const double
   }
 }
 
-// coarse classes of the owned coarse cube layers [CK0, CK1) of a replicated level
-__global__ void k_coarsen_part(DGrid gf, DGrid gc, int CK0, int CK1, uint8_t* __restrict__ cls_c) {
-  const int nc = gc.n;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (tid >= (int64_t)(CK1 - CK0) * nc * nc * 6) return;
-  const int T = (int)(tid % 6);
-  int64_t r = tid / 6;
-  const int CI = (int)(r % nc);
-  r /= nc;
-  const int CJ = (int)(r % nc);
-  const int CK = CK0 + (int)(r / nc);
-  uint8_t cl[8];
-  int cnt[8];
-  for (int q = 0; q < 8; ++q) {
-    const int off = c_child_off[T][q];
-    cl[q] = elem_class(gf, 2 * CI + (off & 1), 2 * CJ + ((off >> 1) & 1), 2 * CK + ((off >> 2) & 1),
-                       c_child_t[T][q]);
+// loopback allreduce: out = sum over ranks q = 0..P-1 (in that order) of in[q][0..count)
+__global__ void k_loopback_sum(const double* const* __restrict__ in, int P, int count, double* __restrict__ out) {
+  for (int c = threadIdx.x; c < count; c += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < P; ++q) s += in[q][c];
+    out[c] = s;
   }
-  for (int q = 0; q < 8; ++q) {
-    cnt[q] = 0;
-    for (int s = 0; s < 8; ++s) cnt[q] += cl[s] == cl[q];
-  }
-  int best = 0;
-  for (int q = 1; q < 8; ++q) {
-    const bool better = cnt[q] > cnt[best] ||
-                        (cnt[q] == cnt[best] && (mu_of(gf, cl[q]) > mu_of(gf, cl[best]) ||
-                                                 (mu_of(gf, cl[q]) == mu_of(gf, cl[best]) && cl[q] < cl[best])));
-    if (better) best = q;
-  }
-  cls_c[((((int64_t)(CK - gc.cz0)) * nc + CJ) * nc + CI) * 6 + T] = cl[best];
 }
+
+}  // namespace stk
+
+// the loopback group (opaque in stk.h): a host barrier plus published pointers
+struct stk_loopback {
+  int P = 1;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long generation = 0;
+  std::vector<void*> ptr;      // published by each rank at a rendezvous
+  std::vector<int64_t> aux;    // e.g. the rank's field stride / plane count
+  double** dptrs = nullptr;    // device copy of ptr (allreduce)
+  double* dsum = nullptr;      // device result of the allreduce
+  double** hp = nullptr;       // pinned host staging of the pointer table
+  void* stream = nullptr;      // the one CUDA stream every rank's context uses
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long gen = generation;
+    if (++arrived == P) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+
+namespace stk {
+
+#define ST_RET(call)                 \
+  do {                               \
+    stk_status s__ = (call);         \
+    if (s__ != STK_OK) return s__;   \
+  } while (0)
 
 struct Comm {
   int rank = 0, nranks = 1;
+  stk_loopback* lb = nullptr;
 #if STK_HAVE_NCCL
   ncclComm_t nc = nullptr;
 #endif
 
   template <class C>
-  stk_status init(C* ctx, int r, int P, const uint8_t* id) {
+  stk_status init(C* ctx, int r, int P, const uint8_t* id, stk_loopback* group) {
     rank = r;
     nranks = P;
     if (P == 1) return STK_OK;
+    if (group) {
+      if (group->P != P) {
+        ctx->err = "loopback group size differs from cfg.nranks";
+        return STK_EINVAL;
+      }
+      lb = group;
+      return STK_OK;
+    }
 #if STK_HAVE_NCCL
     if (!id) {
       ctx->err = "nranks > 1 needs the NCCL unique id";
@@ -106,6 +143,8 @@ struct Comm {
 #endif
   }
 
+  bool loopback() const { return lb != nullptr; }
+
   void destroy() {
 #if STK_HAVE_NCCL
     if (nc) ncclCommDestroy(nc);
@@ -113,11 +152,48 @@ struct Comm {
 #endif
   }
 
+  // rendezvous: publish (p, a), wait for all ranks
+  void publish(void* p, int64_t a = 0) {
+    lb->ptr[rank] = p;
+    lb->aux[rank] = a;
+    lb->barrier();
+  }
+
+  template <class C>
+  static stk_status cuda_ok(C* ctx, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return STK_OK;
+    ctx->err = std::string(what) + ": " + cudaGetErrorString(e);
+    return STK_ECUDA;
+  }
+
   // exchange the boundary planes of fields [f0, f0+nf) of a distributed level vector
+  // (fs: this rank's field stride; py: plane pitch, equal on all ranks)
   template <class C>
   stk_status halo(C* ctx, int n, int z0, int nzl, int64_t py, int64_t fs, double* v, int f0, int nf,
                   bool replicated) {
     if (nranks == 1 || replicated) return STK_OK;
+    (void)n; (void)z0;
+    if (lb) {
+      // publish (v, fs); a rank's own planes 1..nzl, halos 0 and nzl+1
+      publish(v, fs);
+      stk_status st = STK_OK;
+      for (int f = f0; f < f0 + nf && st == STK_OK; ++f) {
+        double* base = v + f * fs;
+        if (rank > 0) {  // top owned plane of rank-1 -> my plane 0
+          const double* pb = (const double*)lb->ptr[rank - 1] + f * lb->aux[rank - 1];
+          // rank-1 owns exactly (n/P) planes (it is not the last rank): its top plane index is that
+          st = cuda_ok(ctx, cudaMemcpyAsync(base, pb + (int64_t)nzl_below(n) * py, sizeof(double) * py,
+                                            cudaMemcpyDeviceToDevice, ctx->stream), "loopback halo");
+        }
+        if (st == STK_OK && rank < nranks - 1) {  // first owned plane of rank+1 -> my plane nzl+1
+          const double* pa = (const double*)lb->ptr[rank + 1] + f * lb->aux[rank + 1];
+          st = cuda_ok(ctx, cudaMemcpyAsync(base + (int64_t)(nzl + 1) * py, pa + py, sizeof(double) * py,
+                                            cudaMemcpyDeviceToDevice, ctx->stream), "loopback halo");
+        }
+      }
+      lb->barrier();
+      return st;
+    }
 #if STK_HAVE_NCCL
     ncclGroupStart();
     for (int f = f0; f < f0 + nf; ++f) {
@@ -136,20 +212,109 @@ struct Comm {
       ctx->err = std::string("halo exchange: ") + ncclGetErrorString(res);
       return STK_ENCCL;
     }
-    (void)n; (void)z0;
+    return STK_OK;
+#else
+    return STK_EUNSUP;
+#endif
+  }
+  // planes owned by a rank below the last one (the slab partition gives every rank
+  // but the last n_l / P planes)
+  int nzl_below(int n) const { return n / nranks; }
+
+  // d[0..count) = sum over ranks (count <= 256)
+  template <class C>
+  stk_status allreduce_sum(C* ctx, double* d, int count) {
+    if (nranks == 1) return STK_OK;
+    if (lb) {
+      publish(d);
+      stk_status st = STK_OK;
+      if (rank == 0) {
+        for (int q = 0; q < nranks; ++q) lb->hp[q] = (double*)lb->ptr[q];
+        st = cuda_ok(ctx, cudaMemcpyAsync(lb->dptrs, lb->hp, sizeof(double*) * nranks, cudaMemcpyHostToDevice,
+                                          ctx->stream), "loopback allreduce");
+        if (st == STK_OK) {
+          k_loopback_sum<<<1, 32, 0, ctx->stream>>>(lb->dptrs, nranks, count, lb->dsum);
+          st = cuda_ok(ctx, cudaGetLastError(), "loopback allreduce");
+        }
+      }
+      lb->barrier();  // the sum is enqueued (stream order) before every rank's copy out
+      if (st == STK_OK)
+        st = cuda_ok(ctx, cudaMemcpyAsync(d, lb->dsum, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream),
+                     "loopback allreduce");
+      lb->barrier();  // dsum / the pointer table are not reused before every copy is enqueued
+      return st;
+    }
+#if STK_HAVE_NCCL
+    ncclResult_t res = ncclAllReduce(d, d, count, ncclDouble, ncclSum, nc, ctx->stream);
+    if (res != ncclSuccess) {
+      ctx->err = std::string("allreduce: ") + ncclGetErrorString(res);
+      return STK_ENCCL;
+    }
     return STK_OK;
 #else
     return STK_EUNSUP;
 #endif
   }
 
-  template <class C>
-  stk_status allreduce_sum(C* ctx, double* d, int count) {
+  // every rank holds a buffer of the same layout; rank q owns the byte range
+  // [off(q), off(q) + len(q)); afterwards every rank holds every range
+  template <class C, class R>
+  stk_status allgather_ranges(C* ctx, uint8_t* base, const R& range) {
     if (nranks == 1) return STK_OK;
+    if (lb) {
+      publish(base);
+      stk_status st = STK_OK;
+      for (int q = 0; q < nranks && st == STK_OK; ++q) {
+        if (q == rank) continue;
+        int64_t off, len;
+        range(q, off, len);
+        if (len <= 0) continue;
+        st = cuda_ok(ctx, cudaMemcpyAsync(base + off, (const uint8_t*)lb->ptr[q] + off, (size_t)len,
+                                          cudaMemcpyDeviceToDevice, ctx->stream), "loopback gather");
+      }
+      lb->barrier();
+      return st;
+    }
 #if STK_HAVE_NCCL
-    ncclResult_t res = ncclAllReduce(d, d, count, ncclDouble, ncclSum, nc, ctx->stream);
+    ncclGroupStart();
+    for (int q = 0; q < nranks; ++q) {
+      int64_t off, len;
+      range(q, off, len);
+      if (len <= 0) continue;
+      ncclBroadcast(base + off, base + off, (size_t)len, ncclUint8, q, nc, ctx->stream);
+    }
+    ncclResult_t res = ncclGroupEnd();
     if (res != ncclSuccess) {
-      ctx->err = std::string("allreduce: ") + ncclGetErrorString(res);
+      ctx->err = std::string("gather: ") + ncclGetErrorString(res);
+      return STK_ENCCL;
+    }
+    return STK_OK;
+#else
+    return STK_EUNSUP;
+#endif
+  }
+
+  // rank r < P-1 sends bytes [src_off, src_off + len) of its buffer to rank r+1, which
+  // receives them at [0, len) of its own (the lowest stored cube layer)
+  template <class C>
+  stk_status shift_up(C* ctx, uint8_t* base, int64_t src_off, int64_t len) {
+    if (nranks == 1) return STK_OK;
+    if (lb) {
+      publish(base, src_off);
+      stk_status st = STK_OK;
+      if (rank > 0)
+        st = cuda_ok(ctx, cudaMemcpyAsync(base, (const uint8_t*)lb->ptr[rank - 1] + lb->aux[rank - 1], (size_t)len,
+                                          cudaMemcpyDeviceToDevice, ctx->stream), "loopback layer");
+      lb->barrier();
+      return st;
+    }
+#if STK_HAVE_NCCL
+    ncclGroupStart();
+    if (rank < nranks - 1) ncclSend(base + src_off, (size_t)len, ncclUint8, rank + 1, nc, ctx->stream);
+    if (rank > 0) ncclRecv(base, (size_t)len, ncclUint8, rank - 1, nc, ctx->stream);
+    ncclResult_t res = ncclGroupEnd();
+    if (res != ncclSuccess) {
+      ctx->err = std::string("layer exchange: ") + ncclGetErrorString(res);
       return STK_ENCCL;
     }
     return STK_OK;
@@ -174,58 +339,21 @@ struct Comm {
     const int64_t work = nx * nx * (K1 - K0);
     if (work > 0) k_restrict_part<<<(unsigned)((work + 255) / 256), 256, 0, ctx->stream>>>(gf, gc, K0, K1, rf, bc);
     ctx->launches++;
-#if STK_HAVE_NCCL
-    ncclGroupStart();
-    for (int q = 0; q < nranks; ++q) {
-      int a, b;
-      owned_coarse(gf.n, nranks, q, a, b);
-      if (b <= a) continue;
-      for (int f = 0; f < 4; ++f) {
-        double* p = bc + f * gc.fs + (int64_t)(a - gc.z0 + 1) * gc.py;
-        ncclBroadcast(p, p, (size_t)(b - a) * gc.py, ncclDouble, q, nc, ctx->stream);
-      }
-    }
-    ncclResult_t res = ncclGroupEnd();
-    if (res != ncclSuccess) {
-      ctx->err = std::string("coarse gather: ") + ncclGetErrorString(res);
-      return STK_ENCCL;
+    const int P = nranks;
+    const int nf = gf.n;
+    for (int f = 0; f < 4; ++f) {
+      const int64_t fbase = (int64_t)f * gc.fs * 8;
+      ST_RET(allgather_ranges(ctx, (uint8_t*)bc, [&](int q, int64_t& off, int64_t& len) {
+        int a, b;
+        owned_coarse(nf, P, q, a, b);
+        off = fbase + (int64_t)(a - gc.z0 + 1) * gc.py * 8;
+        len = (int64_t)(b - a) * gc.py * 8;
+      }));
     }
     return STK_OK;
-#else
-    return nranks == 1 ? STK_OK : STK_EUNSUP;
-#endif
   }
 
   DGrid replicated_view(DGrid gc) const { return gc; }
-
-  template <class C>
-  stk_status gather_classes(C* ctx, DGrid gf, DGrid gc, uint8_t* cls_c) {
-    // coarse cube layer CK derives from fine cube layers 2CK, 2CK+1: rank q computes
-    // the coarse layers whose fine layers it owns, then broadcasts them
-    const int nc_ = gc.n;
-    const int per = gf.n / nranks;
-    const int CK0 = rank * per / 2, CK1 = (rank + 1) * per / 2;
-    const int64_t work = (int64_t)(CK1 - CK0) * nc_ * nc_ * 6;
-    if (work > 0) k_coarsen_part<<<(unsigned)((work + 255) / 256), 256, 0, ctx->stream>>>(gf, gc, CK0, CK1, cls_c);
-    ctx->launches++;
-#if STK_HAVE_NCCL
-    ncclGroupStart();
-    for (int q = 0; q < nranks; ++q) {
-      const int a = q * per / 2, b = (q + 1) * per / 2;
-      if (b <= a) continue;
-      uint8_t* p = cls_c + (int64_t)a * nc_ * nc_ * 6;
-      ncclBroadcast(p, p, (size_t)(b - a) * nc_ * nc_ * 6, ncclUint8, q, nc, ctx->stream);
-    }
-    ncclResult_t res = ncclGroupEnd();
-    if (res != ncclSuccess) {
-      ctx->err = std::string("class gather: ") + ncclGetErrorString(res);
-      return STK_ENCCL;
-    }
-    return STK_OK;
-#else
-    return nranks == 1 ? STK_OK : STK_EUNSUP;
-#endif
-  }
 };
 
 inline stk_status comm_unique_id(uint8_t id[128]) {

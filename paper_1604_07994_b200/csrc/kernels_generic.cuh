@@ -292,38 +292,47 @@ __global__ void k_unpack(DGrid g, const double* __restrict__ dev, double* __rest
 
 // ---- setup kernels -------------------------------------------------------
 
-// coarse element class = majority class of its 8 Bey children; ties -> larger mu,
-// then smaller class id (DESIGN R15).  gf/gc: fine/coarse grids (cube layers stored).
-__global__ void k_coarsen_classes(DGrid gf, DGrid gc, int ncz, uint8_t* __restrict__ cls_c) {
+// coarse element coefficients of cube layers [CK0, CK1) (reading R15): for the 8 Bey
+// children of each coarse tet, mu_A = arithmetic mean of the children's
+// mu_A (the rediscretised coarse A is then the Galerkin product P^T A P), 1/mu_C = mean
+// of the children's 1/mu_C; the class is the children's common class, else CLS_MIXED.
+// gf/gc: fine/coarse grids (cube layers stored); cls_c / emu_c in gc's layout.
+__global__ void k_coarsen(DGrid gf, DGrid gc, int CK0, int CK1, uint8_t* __restrict__ cls_c,
+                          double2* __restrict__ emu_c) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int nc = gc.n;
-  const int64_t total = (int64_t)ncz * nc * nc * 6;
+  const int64_t total = (int64_t)(CK1 - CK0) * nc * nc * 6;
   if (tid >= total) return;
   const int T = (int)(tid % 6);
   int64_t r = tid / 6;
   const int CI = (int)(r % nc);
   r /= nc;
   const int CJ = (int)(r % nc);
-  const int CK = gc.cz0 + (int)(r / nc);
-  uint8_t cl[8];
-  int cnt[8];
+  const int CK = CK0 + (int)(r / nc);
+  double sm = 0.0, si = 0.0;
+  int c0 = -1;
+  bool pure = true;
   for (int q = 0; q < 8; ++q) {
     const int off = c_child_off[T][q];
-    cl[q] = elem_class(gf, 2 * CI + (off & 1), 2 * CJ + ((off >> 1) & 1), 2 * CK + ((off >> 2) & 1),
-                       c_child_t[T][q]);
+    const int fi = 2 * CI + (off & 1), fj = 2 * CJ + ((off >> 1) & 1), fk = 2 * CK + ((off >> 2) & 1);
+    const int ft = c_child_t[T][q];
+    const int cl = elem_class(gf, fi, fj, fk, ft);
+    double mu, imu;
+    tet_coef(gf, fi, fj, fk, ft, cl, mu, imu);
+    sm += mu;
+    si += imu;
+    if (q == 0) c0 = cl;
+    pure = pure && cl == c0 && cl != CLS_MIXED;
   }
-  for (int q = 0; q < 8; ++q) {
-    cnt[q] = 0;
-    for (int s = 0; s < 8; ++s) cnt[q] += cl[s] == cl[q];
-  }
-  int best = 0;
-  for (int q = 1; q < 8; ++q) {
-    const bool better = cnt[q] > cnt[best] ||
-                        (cnt[q] == cnt[best] && (mu_of(gf, cl[q]) > mu_of(gf, cl[best]) ||
-                                                 (mu_of(gf, cl[q]) == mu_of(gf, cl[best]) && cl[q] < cl[best])));
-    if (better) best = q;
-  }
-  cls_c[tid] = cl[best];
+  const int64_t o = elem_index(gc, CI, CJ, CK, T);
+  cls_c[o] = pure ? (uint8_t)c0 : CLS_MIXED;
+  emu_c[o] = make_double2(sm * 0.125, si * 0.125);
+}
+
+// number of entries >= lim (input validation of the element classes)
+__global__ void k_count_ge(const uint8_t* __restrict__ a, int64_t n, int lim, unsigned long long* cnt) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n && a[t] >= lim) atomicAdd(cnt, 1ull);
 }
 
 // per-vertex code (R6): class k (< 0x40) when
@@ -360,6 +369,7 @@ __global__ void k_classify(DGrid g, uint8_t* __restrict__ code, unsigned long lo
           for (int t = 0; t < 6; ++t) {
             if (c_corner_m[corner][t] < 0) continue;
             const int cl = elem_class(g, ci, cj, ck, t);
+            if (cl == CLS_MIXED) same = false;  // coarse tet of several classes: never regular (R15)
             if (first < 0) first = cl;
             else if (cl != first && mu_of(g, cl) != mu_of(g, first)) same = false;
           }
@@ -622,7 +632,8 @@ __device__ __forceinline__ void row_warp(const DGrid& g, int i, int j, int k, co
         else v = (d == s3) ? hinv : 0.0;
         gm[d] = v;
       }
-      const double mu = mu_of(g, cl), imu = imu_of(g, cl);
+      double mu, imu;
+      tet_coef(g, ci, cj, ck, t, cl, mu, imu);
       const double gg = gm[0] * gm[0] + gm[1] * gm[1] + gm[2] * gm[2];
       const double tr = G[0][0] + G[1][1] + G[2][2];
       if (blocks & BLK_A) {

@@ -28,6 +28,7 @@ struct Level {
   int cz0 = 0, cz1 = 0;  // stored cube layers
   int64_t px = 0, py = 0, fs = 0, vlen = 0;
   uint8_t* cls = nullptr;
+  double2* emu = nullptr;  // levels >= 1: per-tet (mu_A, 1/mu_C) means over the Bey children (R15)
   uint8_t* code = nullptr;
   double* x = nullptr;    // MG iterate (levels >= 1)
   double* b = nullptr;    // MG rhs (levels >= 1)
@@ -221,6 +222,7 @@ DGrid dgrid(const stk_ctx* ctx, const Level& L) {
   g.idh3 = 1.0 / (ctx->cfg.delta * L.h * L.h * L.h);
   g.dirmask = dirmask_of(ctx->cfg);
   g.cls = L.cls;
+  g.emu = L.emu;
   g.code = L.code;
   g.mu = ctx->d_mu;
   return g;
@@ -690,7 +692,8 @@ stk_status op_coarse_part(stk_ctx* ctx) {
   Level& C = ctx->lev[1];
   static const bool no_graph = getenv("STK_NO_GRAPH") && atoi(getenv("STK_NO_GRAPH"));
   if (ctx->fl == 1) return op_fused(ctx);  // one launch: nothing to capture
-  if (ctx->prof.on == 2 || no_graph) {
+  // (the loopback exchanger's host rendezvous cannot be captured: launch directly)
+  if (ctx->prof.on == 2 || no_graph || ctx->comm.loopback()) {
     CK(cudaMemsetAsync(C.x, 0, sizeof(double) * C.vlen, ctx->stream));
     return op_vcycle(ctx, 1, C.b, C.x);
   }
@@ -761,8 +764,8 @@ stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x) {
 
 constexpr int kDotBlocks = 296;
 
-// host out[q] = <V_q, w> over owned entries, all ranks (synchronises)
-stk_status op_dots(stk_ctx* ctx, const double* V, int nv, const double* w, double* out) {
+// dev out[q] = <V_q, w> over owned entries, all ranks (stream-ordered, no host sync)
+stk_status op_dots_dev(stk_ctx* ctx, const double* V, int nv, const double* w, double* out) {
   Level& L = ctx->lev[0];
   DGrid g = dgrid(ctx, L);
   PScope ps(ctx, P_KRYLOV, 0);
@@ -770,29 +773,40 @@ stk_status op_dots(stk_ctx* ctx, const double* V, int nv, const double* w, doubl
     const int m = std::min(KRY_CHUNK, nv - c0);
     k_dots<<<kDotBlocks, 256, 0, ctx->stream>>>(g, V + (int64_t)c0 * L.vlen, L.vlen, m, w, ctx->kpart);
     ST(launched(ctx));
-    k_dots_final<<<1, 32, 0, ctx->stream>>>(ctx->kpart, kDotBlocks, m, ctx->kcoef + c0);
+    k_dots_final<<<1, 32, 0, ctx->stream>>>(ctx->kpart, kDotBlocks, m, out + c0);
     ST(launched(ctx));
   }
-  if (!L.replicated) ST(ctx->comm.allreduce_sum(ctx, ctx->kcoef, nv));
+  if (!L.replicated) ST(ctx->comm.allreduce_sum(ctx, out, nv));
+  return STK_OK;
+}
+
+// host out[q] = <V_q, w> (synchronises)
+stk_status op_dots(stk_ctx* ctx, const double* V, int nv, const double* w, double* out) {
+  ST(op_dots_dev(ctx, V, nv, w, ctx->kcoef));
   CK(cudaMemcpyAsync(out, ctx->kcoef, sizeof(double) * nv, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return STK_OK;
 }
 
-// w = alpha w - sum_q c[q] V_q  (c on the host)
-stk_status op_update(stk_ctx* ctx, const double* V, int nv, const double* c, double alpha, double* w) {
+// w = alpha w - sum_q c[q] V_q, coefficients c on the device
+stk_status op_update_dev(stk_ctx* ctx, const double* V, int nv, const double* c, double alpha, double* w) {
   Level& L = ctx->lev[0];
   DGrid g = dgrid(ctx, L);
   PScope ps(ctx, P_KRYLOV, 0);
-  CK(cudaMemcpyAsync(ctx->kcoef, c, sizeof(double) * nv, cudaMemcpyHostToDevice, ctx->stream));
   for (int c0 = 0; c0 < nv || c0 == 0; c0 += KRY_CHUNK) {
     const int m = std::min(KRY_CHUNK, nv - c0);
     k_update<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(g, V + (int64_t)c0 * L.vlen, L.vlen, m,
-                                                                         ctx->kcoef + c0, c0 == 0 ? alpha : 1.0, w);
+                                                                         c + c0, c0 == 0 ? alpha : 1.0, w);
     ST(launched(ctx));
     if (nv == 0) break;
   }
   return STK_OK;
+}
+
+// w = alpha w - sum_q c[q] V_q  (c on the host)
+stk_status op_update(stk_ctx* ctx, const double* V, int nv, const double* c, double alpha, double* w) {
+  CK(cudaMemcpyAsync(ctx->kcoef, c, sizeof(double) * nv, cudaMemcpyHostToDevice, ctx->stream));
+  return op_update_dev(ctx, V, nv, ctx->kcoef, alpha, w);
 }
 
 stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x);
@@ -808,7 +822,7 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
   const size_t vb = sizeof(double) * vlen;
   if (!ctx->kbasis) {
     if (cudaMalloc(&ctx->kbasis, vb * (m + 1)) != cudaSuccess || cudaMalloc(&ctx->kwork, vb * 3) != cudaSuccess ||
-        cudaMalloc(&ctx->kcoef, sizeof(double) * (m + 2 + KRY_CHUNK)) != cudaSuccess ||
+        cudaMalloc(&ctx->kcoef, sizeof(double) * (3 * (m + 2) + KRY_CHUNK)) != cudaSuccess ||
         cudaMalloc(&ctx->kpart, sizeof(double) * kDotBlocks * KRY_CHUNK) != cudaSuccess) {
       cudaGetLastError();
       ctx->err = "out of device memory for the GMRES basis (reduce cfg.krylov)";
@@ -839,14 +853,21 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
       CK(cudaMemsetAsync(z, 0, vb, ctx->stream));
       ST(op_vcycle(ctx, 0, V(j), z));
       ST(op_apply(ctx, 0, BLK_ALL, z, w));
-      ST(op_dots(ctx, V(0), j + 1, w, h.data()));
-      ST(op_update(ctx, V(0), j + 1, h.data(), 1.0, w));
-      ST(op_dots(ctx, V(0), j + 1, w, h2.data()));
-      ST(op_update(ctx, V(0), j + 1, h2.data(), 1.0, w));
-      for (int q = 0; q <= j; ++q) h[q] += h2[q];
-      double ww;
-      ST(op_dots(ctx, w, 1, w, &ww));
-      h[j + 1] = std::sqrt(ww);
+      // classical Gram-Schmidt twice (CGS2) with the coefficients kept on the device;
+      // one host round trip per iteration for the Hessenberg column and ||w||
+      double* c1 = ctx->kcoef + (m + 2);
+      double* c2 = ctx->kcoef + 2 * (m + 2);
+      ST(op_dots_dev(ctx, V(0), j + 1, w, c1));
+      ST(op_update_dev(ctx, V(0), j + 1, c1, 1.0, w));
+      ST(op_dots_dev(ctx, V(0), j + 1, w, c2));
+      ST(op_update_dev(ctx, V(0), j + 1, c2, 1.0, w));
+      ST(op_dots_dev(ctx, w, 1, w, c2 + (j + 1)));
+      std::vector<double> hc(2 * (m + 2));
+      CK(cudaMemcpyAsync(hc.data(), c1, sizeof(double) * 2 * (m + 2), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      for (int q = 0; q <= j; ++q) h[q] = hc[q] + hc[(m + 2) + q];
+      const double ww = hc[(m + 2) + j + 1];
+      h[j + 1] = std::sqrt(std::max(ww, 0.0));
       if (h[j + 1] > 0) {
         k_axpby<<<nb, kThreads, 0, ctx->stream>>>(g0, 1.0 / h[j + 1], w, 0.0, V(j + 1));
         ST(launched(ctx));
@@ -1062,7 +1083,56 @@ stk_status stk_partition(int32_t n, int32_t n_coarse, int32_t nranks, int32_t ra
   return STK_OK;
 }
 
+namespace {
+stk_status create_impl(const stk_config* cfg, const uint8_t* id, stk_loopback* group, stk_ctx** out);
+}
+
 stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
+  return create_impl(cfg, id, nullptr, out);
+}
+
+stk_status stk_loopback_create(int32_t nranks, stk_loopback** out) {
+  if (!out || nranks < 1 || nranks > 64) return STK_EINVAL;
+  stk_loopback* g = new stk_loopback();
+  g->P = nranks;
+  g->ptr.assign(nranks, nullptr);
+  g->aux.assign(nranks, 0);
+  if (cudaMalloc(&g->dptrs, sizeof(double*) * nranks) != cudaSuccess ||
+      cudaMalloc(&g->dsum, sizeof(double) * 256) != cudaSuccess ||
+      cudaMallocHost(&g->hp, sizeof(double*) * nranks) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(g->dptrs);
+    cudaFree(g->dsum);
+    delete g;
+    return STK_ENOMEM;
+  }
+  *out = g;
+  return STK_OK;
+}
+
+stk_status stk_loopback_destroy(stk_loopback* g) {
+  if (!g) return STK_EINVAL;
+  cudaFree(g->dptrs);
+  cudaFree(g->dsum);
+  cudaFreeHost(g->hp);
+  delete g;
+  return STK_OK;
+}
+
+stk_status stk_create_loopback(const stk_config* cfg, stk_loopback* group, stk_ctx** out) {
+  if (!group || !cfg) return STK_EINVAL;
+  {
+    std::lock_guard<std::mutex> lk(group->m);
+    if (!group->stream) group->stream = cfg->stream ? cfg->stream : (void*)1;
+    else if (group->stream != (cfg->stream ? cfg->stream : (void*)1)) return STK_EINVAL;  // one stream for all ranks
+  }
+  return create_impl(cfg, nullptr, group, out);
+}
+
+}  // extern "C"
+
+namespace {
+stk_status create_impl(const stk_config* cfg, const uint8_t* id, stk_loopback* group, stk_ctx** out) {
   if (!cfg || !out) return STK_EINVAL;
   *out = nullptr;
   const int n = cfg->n;
@@ -1096,7 +1166,7 @@ stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
     return fail(STK_ECUDA);
   }
   // communicator
-  stk_status s = ctx->comm.init(ctx, cfg->rank, cfg->nranks, id);
+  stk_status s = ctx->comm.init(ctx, cfg->rank, cfg->nranks, id, group);
   if (s != STK_OK) return fail(s);
   // levels
   for (int m = n; m >= nc; m /= 2) {
@@ -1117,7 +1187,11 @@ stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
     L.cz1 = part[l].cz1;
     L.px = ((L.n + 3 + 15) / 16) * 16;  // ghost column i = -1, vertices 0..n, spare
     L.py = L.px * (L.n + 2);             // ghost row j = -1, rows 0..n
-    L.fs = (((int64_t)(L.nzl + 2) * L.py + 31) / 32) * 32;
+    // planes z0-1 .. z0+nzl (halos included) plus one spare plane: the row kernels
+    // gather the Kuhn offset (0,1,1) of a vertex on the top-back edge without bounds
+    // checks, i.e. row j = n+1 of the top halo plane = the spare plane's ghost row
+    // (0 by the level-vector invariant) -- without it that read left the field
+    L.fs = (((int64_t)(L.nzl + 3) * L.py + 31) / 32) * 32;
     L.vlen = 4 * L.fs;
     const size_t ncls = (size_t)(L.cz1 - L.cz0) * L.n * L.n * 6;
     if (cudaMalloc(&L.cls, ncls) != cudaSuccess ||
@@ -1129,6 +1203,10 @@ stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
     cudaMemset(L.r, 0, sizeof(double) * L.vlen);
     cudaMemset(L.code, CODE_IRREGULAR, L.fs);
     if (l > 0) {
+      if (cudaMalloc(&L.emu, sizeof(double2) * ncls) != cudaSuccess) {
+        ctx->err = "out of device memory (coarse element coefficients)";
+        return fail(STK_ENOMEM);
+      }
       if (cudaMalloc(&L.x, sizeof(double) * L.vlen) != cudaSuccess ||
           cudaMalloc(&L.b, sizeof(double) * L.vlen) != cudaSuccess) {
         ctx->err = "out of device memory (MG vectors)";
@@ -1154,6 +1232,9 @@ stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
   *out = ctx;
   return STK_OK;
 }
+}  // namespace
+
+extern "C" {
 
 stk_status stk_cube_range(const stk_ctx* ctx, int32_t* z0, int32_t* z1) {
   if (!ctx || !z0 || !z1) return STK_EINVAL;
@@ -1165,7 +1246,7 @@ stk_status stk_cube_range(const stk_ctx* ctx, int32_t* z0, int32_t* z1) {
 stk_status stk_set_viscosity(stk_ctx* ctx, const uint8_t* elem_class, const double* class_mu,
                              int32_t nclass) {
   ST(check(ctx, 0));
-  if (!elem_class || !class_mu || nclass < 1 || nclass > 255) return STK_EINVAL;
+  if (!elem_class || !class_mu || nclass < 1 || nclass > 254) return STK_EINVAL;  // 0xFE, 0xFF reserved
   double mu[256], imu[256];
   for (int q = 0; q < 256; ++q) mu[q] = imu[q] = 1.0;
   for (int q = 0; q < nclass; ++q) {
@@ -1184,7 +1265,17 @@ stk_status stk_set_viscosity(stk_ctx* ctx, const uint8_t* elem_class, const doub
   Level& L = ctx->lev[0];
   const size_t ncls = (size_t)(L.cz1 - L.cz0) * L.n * L.n * 6;
   CK(cudaMemcpyAsync(L.cls, elem_class, ncls, cudaMemcpyHostToDevice, ctx->stream));
+  if (!ctx->dcnt) CK(cudaMalloc(&ctx->dcnt, sizeof(unsigned long long) * (ctx->nlev + 1)));
+  CK(cudaMemsetAsync(ctx->dcnt, 0, sizeof(unsigned long long), ctx->stream));
+  k_count_ge<<<nblocks((int64_t)ncls), kThreads, 0, ctx->stream>>>(L.cls, (int64_t)ncls, nclass, ctx->dcnt);
+  ST(launched(ctx));
+  unsigned long long bad = 0;
+  CK(cudaMemcpyAsync(&bad, ctx->dcnt, sizeof(bad), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  if (bad) {
+    ctx->err = "element class >= nclass";
+    return STK_EINVAL;
+  }
   ctx->state = std::max(ctx->state, 1);
   if (ctx->state > 1) ctx->state = 1;  // re-assemble required
   return STK_OK;
@@ -1192,17 +1283,46 @@ stk_status stk_set_viscosity(stk_ctx* ctx, const uint8_t* elem_class, const doub
 
 stk_status stk_assemble(stk_ctx* ctx) {
   ST(check(ctx, 1));
-  // coarse classes
+  // coarse element classes and coefficients (R15), finest to coarsest
+  const int P = ctx->cfg.nranks, rank = ctx->cfg.rank;
   for (int l = 1; l < ctx->nlev; ++l) {
     Level& F = ctx->lev[l - 1];
     Level& C = ctx->lev[l];
+    const int64_t lay = (int64_t)C.n * C.n * 6;  // tets per cube layer
+    auto coarsen = [&](int CK0, int CK1) -> stk_status {
+      const int64_t tot = (int64_t)(CK1 - CK0) * lay;
+      if (tot <= 0) return STK_OK;
+      k_coarsen<<<nblocks(tot), kThreads, 0, ctx->stream>>>(dgrid(ctx, F), dgrid(ctx, C), CK0, CK1, C.cls, C.emu);
+      return launched(ctx);
+    };
     if (C.replicated && !F.replicated) {
-      ST(ctx->comm.gather_classes(ctx, dgrid(ctx, F), dgrid(ctx, C), C.cls));
+      // coarse layer CK derives from fine layers 2CK, 2CK+1: every rank computes the
+      // coarse layers of its fine slab, then the layers are gathered on every rank
+      const int per = F.n / P;
+      ST(coarsen(rank * per / 2, (rank + 1) * per / 2));
+      auto rng = [&](int64_t esz) {
+        return [=](int q, int64_t& off, int64_t& len) {
+          off = (int64_t)(q * per / 2) * lay * esz;
+          len = (int64_t)((q + 1) * per / 2 - q * per / 2) * lay * esz;
+        };
+      };
+      ST(ctx->comm.allgather_ranges(ctx, C.cls, rng(1)));
+      ST(ctx->comm.allgather_ranges(ctx, (uint8_t*)C.emu, rng(sizeof(double2))));
+    } else if (C.replicated || P == 1 || C.cz0 == C.z0) {
+      ST(coarsen(C.cz0, C.cz1));
+      if (!C.replicated && P > 1) {  // rank 0 of a split level still sends its top layer up
+        ST(ctx->comm.shift_up(ctx, C.cls, (C.cz1 - 1 - C.cz0) * lay, lay));
+        ST(ctx->comm.shift_up(ctx, (uint8_t*)C.emu, (C.cz1 - 1 - C.cz0) * lay * (int64_t)sizeof(double2),
+                              lay * (int64_t)sizeof(double2)));
+      }
     } else {
-      const int ncz = C.cz1 - C.cz0;
-      const int64_t tot = (int64_t)ncz * C.n * C.n * 6;
-      k_coarsen_classes<<<nblocks(tot), kThreads, 0, ctx->stream>>>(dgrid(ctx, F), dgrid(ctx, C), ncz, C.cls);
-      ST(launched(ctx));
+      // split level, rank > 0: the layers of the own fine slab [z0, cz1); the lowest
+      // stored layer z0 - 1 (needs fine layer 2 z0 - 2, not stored here) comes from
+      // rank - 1, whose top computed layer it is
+      ST(coarsen(C.z0, C.cz1));
+      ST(ctx->comm.shift_up(ctx, C.cls, (C.cz1 - 1 - C.cz0) * lay, lay));
+      ST(ctx->comm.shift_up(ctx, (uint8_t*)C.emu, (C.cz1 - 1 - C.cz0) * lay * (int64_t)sizeof(double2),
+                            lay * (int64_t)sizeof(double2)));
     }
   }
   // classification
@@ -1409,7 +1529,7 @@ stk_status stk_load_vector(stk_ctx* ctx, int32_t kind, const void* f_dev, const 
   Level& L = ctx->lev[0];
   DGrid g = dgrid(ctx, L);
   if (kind == 0) {
-    ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, (double*)f_dev, 0, 3, false));
+    ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, (double*)f_dev, 0, 3, L.replicated));
     k_load_nodal<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(g, (const double*)f_dev, b_dev);
     return launched(ctx);
   }
@@ -1447,7 +1567,16 @@ stk_status stk_residual(stk_ctx* ctx, int32_t level, const double* x, const doub
                         double* norms) {
   ST(check(ctx, 2));
   ST(check_level(ctx, level));
-  ST(op_residual(ctx, level, x, b, r));
+  static const bool dbg_rows = getenv("STK_DBG_ROWS") && atoi(getenv("STK_DBG_ROWS"));
+  if (dbg_rows && row_level(ctx, level)) {
+    Level& L = ctx->lev[level];
+    CK(cudaMemcpyAsync(L.x, x, sizeof(double) * L.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(L.b, b, sizeof(double) * L.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    ST(op_residual_rows(ctx, level));
+    CK(cudaMemcpyAsync(r, L.r, sizeof(double) * L.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    ST(op_residual(ctx, level, x, b, r));
+  }
   if (norms) return stk_norms(ctx, level, r, norms);
   return STK_OK;
 }
@@ -1456,6 +1585,25 @@ stk_status stk_smooth(stk_ctx* ctx, int32_t level, double* x, const double* b, i
   ST(check(ctx, 2));
   ST(check_level(ctx, level));
   if (level == ctx->nlev - 1 && ctx->nlev > 1) { /* allowed: smoothing on the coarsest grid */ }
+  static const bool dbg_rows = getenv("STK_DBG_ROWS") && atoi(getenv("STK_DBG_ROWS"));
+  static const int dbg_coarse = getenv("STK_DBG_COARSE") ? atoi(getenv("STK_DBG_COARSE")) : 0;
+  if (dbg_coarse && level == ctx->nlev - 1) {  // debug: the coarse solve (1: row kernel, 2: one-CTA kernel)
+    Level& L = ctx->lev[level];
+    CK(cudaMemcpyAsync(L.b, b, sizeof(double) * L.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemsetAsync(L.x, 0, sizeof(double) * L.vlen, ctx->stream));
+    if (dbg_coarse == 1) ST(op_coarse_rows(ctx));
+    else ST(op_coarse(ctx, L.b, L.x));
+    CK(cudaMemcpyAsync(x, L.x, sizeof(double) * L.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    return STK_OK;
+  }
+  if (dbg_rows && row_level(ctx, level)) {  // debug: the V-cycle's row kernels on the caller's vectors
+    Level& L = ctx->lev[level];
+    CK(cudaMemcpyAsync(L.x, x, sizeof(double) * L.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(L.b, b, sizeof(double) * L.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    for (int s = 0; s < steps; ++s) ST(op_uzawa_rows(ctx, level));
+    CK(cudaMemcpyAsync(x, L.x, sizeof(double) * L.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    return STK_OK;
+  }
   for (int s = 0; s < steps; ++s) ST(op_uzawa(ctx, level, x, b));
   return STK_OK;
 }
@@ -1463,12 +1611,31 @@ stk_status stk_smooth(stk_ctx* ctx, int32_t level, double* x, const double* b, i
 stk_status stk_restrict(stk_ctx* ctx, int32_t fine_level, const double* r_f, double* b_c) {
   ST(check(ctx, 2));
   if (fine_level < 0 || fine_level >= ctx->nlev - 1) return STK_EINVAL;
+  static const bool dbg_rows = getenv("STK_DBG_ROWS") && atoi(getenv("STK_DBG_ROWS"));
+  if (dbg_rows && row_level(ctx, fine_level) && row_level(ctx, fine_level + 1)) {
+    Level& F = ctx->lev[fine_level];
+    Level& C = ctx->lev[fine_level + 1];
+    CK(cudaMemcpyAsync(F.r, r_f, sizeof(double) * F.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    ST(op_restrict_rows(ctx, fine_level));
+    CK(cudaMemcpyAsync(b_c, C.b, sizeof(double) * C.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    return STK_OK;
+  }
   return op_restrict(ctx, fine_level, r_f, b_c);
 }
 
 stk_status stk_prolong_add(stk_ctx* ctx, int32_t coarse_level, const double* x_c, double* x_f) {
   ST(check(ctx, 2));
   if (coarse_level < 1 || coarse_level >= ctx->nlev) return STK_EINVAL;
+  static const bool dbg_rows = getenv("STK_DBG_ROWS") && atoi(getenv("STK_DBG_ROWS"));
+  if (dbg_rows && row_level(ctx, coarse_level - 1) && row_level(ctx, coarse_level)) {
+    Level& F = ctx->lev[coarse_level - 1];
+    Level& C = ctx->lev[coarse_level];
+    CK(cudaMemcpyAsync(C.x, x_c, sizeof(double) * C.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(F.x, x_f, sizeof(double) * F.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    ST(op_prolong_rows(ctx, coarse_level));
+    CK(cudaMemcpyAsync(x_f, F.x, sizeof(double) * F.vlen, cudaMemcpyDeviceToDevice, ctx->stream));
+    return STK_OK;
+  }
   return op_prolong_add(ctx, coarse_level, x_c, x_f);
 }
 
@@ -1535,6 +1702,41 @@ stk_status stk_solve(stk_ctx* ctx, const double* b, double* x, double rtol, int3
                : 0.0;
   if (!(rel <= rtol)) st = STK_ENOCONV;
   return st;
+}
+
+stk_status stk_export_classes(stk_ctx* ctx, int32_t level, uint8_t* cls_host, double* emu_host) {
+  ST(check(ctx, 2));
+  ST(check_level(ctx, level));
+  if (!cls_host) return STK_EINVAL;
+  Level& L = ctx->lev[level];
+  const size_t ncls = (size_t)(L.cz1 - L.cz0) * L.n * L.n * 6;
+  CK(cudaMemcpyAsync(cls_host, L.cls, ncls, cudaMemcpyDeviceToHost, ctx->stream));
+  if (emu_host) {
+    if (L.emu) {
+      CK(cudaMemcpyAsync(emu_host, L.emu, sizeof(double2) * ncls, cudaMemcpyDeviceToHost, ctx->stream));
+    } else {
+      memset(emu_host, 0, sizeof(double2) * ncls);
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return STK_OK;
+}
+
+stk_status stk_export_codes(stk_ctx* ctx, int32_t level, uint8_t* code_host) {
+  ST(check(ctx, 2));
+  ST(check_level(ctx, level));
+  if (!code_host) return STK_EINVAL;
+  Level& L = ctx->lev[level];
+  std::vector<uint8_t> pad((size_t)L.fs);
+  CK(cudaMemcpyAsync(pad.data(), L.code, (size_t)L.fs, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int64_t nx = L.n + 1;
+  for (int k = 0; k < L.nzl; ++k)
+    for (int j = 0; j <= L.n; ++j)
+      for (int i = 0; i <= L.n; ++i)
+        code_host[((int64_t)k * nx + j) * nx + i] =
+            pad[(size_t)((int64_t)(k + 1) * L.py + (int64_t)(j + 1) * L.px + (i + 1))];
+  return STK_OK;
 }
 
 stk_status stk_set_kernel_mode(stk_ctx* ctx, int32_t mode) {
@@ -1604,6 +1806,7 @@ stk_status stk_destroy(stk_ctx* ctx) {
   if (!ctx) return STK_EINVAL;
   for (auto& L : ctx->lev) {
     cudaFree(L.cls);
+    cudaFree(L.emu);
     cudaFree(L.code);
     cudaFree(L.x);
     cudaFree(L.b);

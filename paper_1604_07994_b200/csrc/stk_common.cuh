@@ -19,6 +19,9 @@ namespace stk {
 enum { FORM_MOD = 0, FORM_SYM = 1, FORM_GRAD = 2 };
 enum { BLK_A = 1, BLK_BT = 2, BLK_B = 4, BLK_C = 8, BLK_ALL = 15 };
 constexpr uint8_t CODE_IRREGULAR = 0xFF;
+// element class of a coarse tet whose Bey children do not share one class
+// (reading R15): its coefficients are the per-tet means in DGrid::emu
+constexpr uint8_t CLS_MIXED = 0xFE;
 
 // Kuhn permutations
 __constant__ int8_t c_perm[6][3];
@@ -58,6 +61,9 @@ struct DGrid {
   const uint8_t* cls;   // element classes [cz - cz0][cj][ci][t]
   const uint8_t* code;  // per-vertex code (plane layout of one field)
   const double* mu;     // per-class viscosity mu_k [0..255], 1/mu_k at mu + 256 (device)
+  // coarse levels: per-tet (mu_A, 1/mu_C) means over the Bey children (reading R15), same
+  // layout as cls; read for CLS_MIXED tets only (a pure tet's pair is its class's)
+  const double2* emu;
 };
 
 __device__ __forceinline__ double mu_of(const DGrid& g, int cl) { return __ldg(g.mu + cl); }
@@ -81,8 +87,24 @@ __device__ __forceinline__ bool is_dirichlet(const DGrid& g, int i, int j, int k
          ((m & 8u) && j == g.n) || ((m & 16u) && k == 0) || ((m & 32u) && k == g.n);
 }
 
+__device__ __forceinline__ int64_t elem_index(const DGrid& g, int ci, int cj, int ck, int t) {
+  return ((((int64_t)(ck - g.cz0)) * g.n + cj) * g.n + ci) * 6 + t;
+}
 __device__ __forceinline__ uint8_t elem_class(const DGrid& g, int ci, int cj, int ck, int t) {
-  return g.cls[((((int64_t)(ck - g.cz0)) * g.n + cj) * g.n + ci) * 6 + t];
+  return g.cls[elem_index(g, ci, cj, ck, t)];
+}
+// (mu_A, 1/mu_C) of tet (ci,cj,ck,t) with class cl: the class table, or the per-tet
+// coarse-level means of a MIXED tet (reading R15)
+__device__ __forceinline__ void tet_coef(const DGrid& g, int ci, int cj, int ck, int t, int cl, double& mu,
+                                         double& imu) {
+  if (cl == CLS_MIXED) {
+    const double2 e = __ldg(g.emu + elem_index(g, ci, cj, ck, t));
+    mu = e.x;
+    imu = e.y;
+  } else {
+    mu = mu_of(g, cl);
+    imu = imu_of(g, cl);
+  }
 }
 
 // Generic row of K = [[A, B^T], [B, -C]] at owned vertex (i,j,k), by the
@@ -154,7 +176,8 @@ __device__ __forceinline__ void row_generic(const DGrid& g, int i, int j, int k,
             gm[s3] = hinv;
           }
           const uint8_t cl = elem_class(g, ci, cj, ck, t);
-          const double mu = mu_of(g, cl), imu = imu_of(g, cl);
+          double mu, imu;
+          tet_coef(g, ci, cj, ck, t, cl, mu, imu);
           const double gg = gm[0] * gm[0] + gm[1] * gm[1] + gm[2] * gm[2];
           const double tr = G[0][0] + G[1][1] + G[2][2];
           if (blocks & BLK_A) {
@@ -286,7 +309,8 @@ __device__ __forceinline__ void row_list(const DGrid& g, int i, int j, int k, co
       } else {
         gm[s3] = hinv;
       }
-      const double mu = mu_of(g, cl), imu = imu_of(g, cl);
+      double mu, imu;
+      tet_coef(g, i - (own & 1), j - ((own >> 1) & 1), k - (own >> 2), t, cl, mu, imu);
       const double gg = gm[0] * gm[0] + gm[1] * gm[1] + gm[2] * gm[2];
       const double tr = G[0][0] + G[1][1] + G[2][2];
       if (blocks & BLK_A) {
@@ -329,7 +353,11 @@ __device__ __forceinline__ double gauge_weight(const DGrid& g, int i, int j, int
         if (ci < 0 || ci >= g.n) continue;
         const int corner = (-dx) | ((-dy) << 1) | ((-dz) << 2);
         for (int t = 0; t < 6; ++t)
-          if (c_corner_m[corner][t] >= 0) w += vq * imu_of(g, elem_class(g, ci, cj, ck, t));
+          if (c_corner_m[corner][t] >= 0) {
+            double mu, imu;
+            tet_coef(g, ci, cj, ck, t, elem_class(g, ci, cj, ck, t), mu, imu);
+            w += vq * imu;
+          }
       }
     }
   }

@@ -131,11 +131,12 @@ def _star_minmax(c):
     return smin, smax, b
 
 
-def _list_rows(c, faces):
-    """Expected list-row mask (R6): the star of tets inside the cube
-    holds more than one class, or the vertex lies on a traction face -- except a
-    vertex of the traction top face z = 1 that lies on no other face (its rows
-    are the truncated constant stencils of the 4 cubes below)."""
+def _row_codes(c, faces):
+    """Expected per-vertex row codes (R6, R15) from the element classes
+    c [k][j][i][t]: class k (< 0x40) when the star of tets inside the cube is one
+    pure class and the vertex is interior or lies only on Dirichlet faces; 0x40 | k
+    for such a star at a vertex of the traction top face z = 1 on no other face;
+    else 0xFF (interface / traction / MIXED / boundary row: explicit stencil)."""
     smin, smax, _ = _star_minmax(c)
     m1 = c.shape[0] + 1
     on = np.zeros((6,) + (m1,) * 3, bool)     # [face][k][j][i]
@@ -147,19 +148,35 @@ def _list_rows(c, faces):
         if int(faces[f]) == 1:
             trac |= on[f]
     top_only = on[5] & (on.sum(axis=0) == 1) & (int(faces[5]) == 1)
-    return (smin != smax) | (trac & ~top_only)
+    pure = (smin == smax) & (smax < 0x40)          # MIXED (0xFE) is never regular
+    code = np.full((m1,) * 3, 0xFF, dtype=np.int64)
+    code[pure & ~trac] = smin[pure & ~trac]
+    code[pure & top_only] = 0x40 | smin[pure & top_only]
+    return code.reshape(-1)
 
 
-@pytest.mark.parametrize("cfgname", ["cfg4", "cfg2"])
-def test_classification_and_coarse_classes(cfgname):
-    n = 64
+@pytest.mark.parametrize("cfgname,n", [("cfg4", 64), ("cfg2", 64), ("cfg3", 64), ("cfg5", 32)])
+def test_classification_and_coarse_classes(cfgname, n):
+    """Integer parity, element by element: coarse classes (pure / MIXED, R15) and the
+    per-vertex row codes of every level; the coarse coefficient means within 1e-15."""
     ctx, cfg, cls, _ = make_ctx(cfgname, n, "mod")
-    assert ctx.layout(0).n_irregular == int(_list_rows(cls.reshape(n, n, n, 6), cfg.faces).sum())
-    # coarse level classes == oracle majority rule, level by level (via the list-row counts)
-    h = mg.Hierarchy(n, cls, cfg.class_mu, cfg.faces)
-    for l, lev in enumerate(h.levels):
-        m = lev.n
-        assert ctx.layout(l).n_irregular == int(_list_rows(lev.cls.reshape(m, m, m, 6), cfg.faces).sum())
+    c = np.asarray(cls, dtype=np.uint8)
+    mu_a = np.asarray(cfg.class_mu, dtype=np.float64)[c]
+    imu_c = 1.0 / mu_a
+    m = n
+    for l in range(ctx.nlev):
+        c_g, emu_g = ctx.export_classes(l)
+        np.testing.assert_array_equal(c_g, c)
+        if l > 0:
+            np.testing.assert_allclose(emu_g[:, 0], mu_a, rtol=1e-15)
+            np.testing.assert_allclose(emu_g[:, 1], imu_c, rtol=1e-15)
+        want = _row_codes(c.reshape(m, m, m, 6).astype(np.int64), cfg.faces)
+        np.testing.assert_array_equal(ctx.export_codes(l).astype(np.int64), want)
+        assert ctx.layout(l).n_irregular == int((want == 0xFF).sum())
+        if l + 1 < ctx.nlev:   # the oracle's coarse level (R15)
+            mu_a, imu_c = mg.coarse_viscosity(m, mu_a, imu_c)
+            c = mg.coarse_classes(m, c)
+            m //= 2
 
 
 @pytest.mark.parametrize("cfgname,form,mode", [("cfg1", "mod", 0), ("cfg2", "mod", 1),
@@ -208,21 +225,62 @@ def test_transfers():
 
 @pytest.mark.parametrize("cfgname,n,form", [("cfg1", 16, "mod"), ("cfg2", 16, "mod"),
                                             ("cfg3", 16, "mod"), ("cfg5", 16, "mod"),
-                                            ("cfg2", 16, "sym"), ("cfg2", 32, "mod")])
+                                            ("cfg2", 16, "sym"), ("cfg2", 32, "mod"),
+                                            ("cfg3", 32, "mod"), ("cfg4", 32, "mod")])
 def test_solve_matches_direct_solution(cfgname, n, form):
     """Converged solve vs the oracle's direct solve (north_star: 1e-8 per field).
     The unresolved high-contrast inclusions (cfg3, cfg5) need the V-cycle as a
     GMRES preconditioner: the plain Uzawa V-cycle diverges there."""
     nc = 4 if form == "sym" else 2
-    kry = 30 if cfgname in ("cfg3", "cfg5") else 0
+    kry = 30 if cfgname in ("cfg3", "cfg4", "cfg5") else 0
     ctx, cfg, cls, fcls = make_ctx(cfgname, n, form, ncolors_u=nc, krylov=kry)
     pr = _oracle_problem(cfg, cls, form)
     b_o, b_g = rhs_oracle_and_gpu(ctx, cfg, cls, fcls, pr)
     x_d = pr.solve_direct(b_o)
-    xg, rep = ctx.solve(b_g, rtol=1e-12, max_cycles=100)
+    xg, rep = ctx.solve(b_g, rtol=1e-12, max_cycles=200)
     assert rep.rel_res <= 1e-12
     err, errs = per_field_rel(ctx.export(xg), x_d.reshape(4, -1))
     assert err <= 1e-8, errs
+
+
+@pytest.mark.parametrize("cfgname,n,kry", [("cfg1", 64, 0), ("cfg2", 64, 0), ("cfg3", 64, 30),
+                                           ("cfg2", 128, 0)])
+def test_solve_on_tiled_levels_matches_oracle_multigrid(cfgname, n, kry):
+    """Converged solve at sizes where the tiled (TMA) kernels run (n >= 64) against
+    the oracle multigrid with element-loop products solved to 1e-13 (plain V-cycles,
+    or GMRES with the V-cycle preconditioner for cfg3, R23): 1e-8 per field after
+    the gauge (north_star)."""
+    from oracle import mg_mf
+    ctx, cfg, cls, fcls = make_ctx(cfgname, n, "mod", krylov=kry)
+    h = mg_mf.MFHierarchy(n, cls, cfg.class_mu, cfg.faces)
+    pr = h.levels[0].prob
+    if cfg.forcing == "nodal":
+        f = synth.nodal_forcing(cfg)
+        b_o = fem.load_nodal_elementwise(n, cfg.faces, f)
+        b_g = ctx.load_nodal(f)
+    else:
+        fe = np.asarray(cfg.force_table)[fcls]
+        b_o = fem.Problem.load_element(_Grid(pr), fe)
+        b_g = ctx.load_element(fcls, cfg.force_table)
+    np.testing.assert_allclose(ctx.export(b_g).reshape(-1), b_o, atol=1e-13 * np.abs(b_o).max())
+    if kry:
+        x_o, rel = h.solve_krylov(b_o, rtol=1e-13, restart=40)
+        assert rel <= 1e-12
+    else:
+        x_o, hist = h.solve(b_o, rtol=1e-13, max_cycles=60)
+        assert hist[-1] <= 1e-13
+    xg, rep = ctx.solve(b_g, rtol=1e-12, max_cycles=200)
+    assert rep.rel_res <= 1e-12
+    err, errs = per_field_rel(ctx.export(xg), x_o.reshape(4, -1))
+    assert err <= 1e-8, errs
+
+
+class _Grid:
+    """oracle.fem.Problem.load_element needs only the grid and the free mask, which a
+    matrix-free level has too."""
+
+    def __init__(self, pr):
+        self.n, self.V, self.h, self.free = pr.n, pr.V, pr.h, pr.free
 
 
 def test_solve_cfg1_rate():

@@ -394,6 +394,14 @@ def test_load_nodal_matches_mass_stencil():
     assert np.abs(b[:3, dmask]).max() == 0.0
 
 
+def test_load_nodal_elementwise_equals_assembled_mass():
+    n = 5
+    pr, _ = _cfg1_problem(n, "mod", faces=synth.TOP_TRACTION)
+    f = np.random.default_rng(12).standard_normal((3, pr.V))
+    np.testing.assert_allclose(fem.load_nodal_elementwise(n, synth.TOP_TRACTION, f), pr.load_nodal(f),
+                               rtol=1e-13, atol=1e-17)
+
+
 def test_load_element_brute_force_and_total():
     # element-constant f: b_{i,a} = sum_{T ni i} f_{T,a} |T| / 4 (R10).  Brute force
     # on one tet, and sum_i b_{i,a} = int f_a when no vertex is constrained.
