@@ -1,29 +1,39 @@
 """bench.py — B200 benchmark of the matrix-free Stokes hot path (arXiv:1604.07994).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload cfg2] [--n N] [--form mod] [--krylov 0]
+                    [--workload cfg3] [--n N] [--form mod] [--krylov M]
 
 One JSON line (rank 0).  A *step* is one pass of the whole hot path
-over the workload: assemble (coarse classes, classification, constant stencils,
-coarse inverse) -> load vector -> one operator apply -> multigrid solve of
-K x = b to relative residual 1e-8 from x = 0.
+over the workload: assemble (coarse coefficients, classification, constant and
+explicit stencils, coarse inverse) -> load vector -> one operator apply ->
+solve of K x = b to relative residual 1e-8 from x = 0 (GMRES(M) right-
+preconditioned by one V_var(3,3) cycle for the unresolved inclusions of cfg3-cfg5,
+DESIGN R23; plain V-cycles for cfg1/cfg2).
 
+* Default workload: BASELINE.json configs[2] (cfg3, n = 256, 67.9 M DoF): the
+  metric's configs quote no size, so the largest config that BASELINE.json puts on
+  one GPU is the N = 1 workload (cfg4 / cfg5 are specified on 8 GPUs).
 * metric / unit: BASELINE.json's metric; `value` = device-timed seconds per step
-  per DoF (DoF = 4 (n+1)^3, the paper's convention), inputs resident in
-  HBM; lower is better.  `apply` reports the operator-apply GDoF/s and HBM GB/s
-  (separate timed loop, L2 flushed before every apply).
-* e2e: the same step through the public API from pinned host buffers (element
-  classes and forcing copied in every step; the residual history read back).
-* roofline: the dominant kernel of the step (by summed device time, CUDA events
-  around every launch on the solver stream during the timed steps) against the
-  measured HBM copy bandwidth in MEASURED_PEAKS.json.
-* cpu_baseline: the oracle (oracle/, test infrastructure) timed on the host on a
-  bounded sample: one V-cycle of the oracle multigrid (plain C element-loop
-  products, all host threads) on the same workload, extrapolated by the GPU's
-  cycle count.  `--impl reference` times the same oracle as the reference arm.
-* Default workload: BASELINE.json configs[1] (n = 128, plane interface with
-  mu1/mu2 = 1e3, traction-free top), form "mod".  --gpus N > 1 (torchrun) shards
-  the grid in z-slabs over N ranks (weak scaling is not used: total work fixed).
+  per DoF (DoF = 4 (n+1)^3), inputs resident in HBM, L2 flushed between
+  steps; lower is better.  `apply` reports the operator-apply GDoF/s and HBM GB/s
+  (separate loop, L2 flushed before every apply; 65 algorithmic B per vertex,
+  SURVEY §8(d)).
+* e2e: the same step through the public API from pinned host buffers: element
+  classes and forcing copied in, and the solution (4 fields, canonical layout)
+  copied back out, every step.
+* roofline: the kernel with the largest summed device time in the step (CUDA
+  events around every launch on the solver stream) against the measured HBM copy
+  bandwidth in MEASURED_PEAKS.json, with SURVEY §8(d)'s algorithmic bytes per
+  vertex (apply 65; a velocity colour pass 40 = half of the 80 B two-colour
+  sweep; pressure passes 48 / 24; residual 97).
+* cpu_baseline: the oracle (oracle/, test infrastructure) timed on this host: its
+  C element-loop apply on the full grid (all threads) and on a slab with one
+  thread; the solve extrapolated by the oracle multigrid's cost in operator
+  applications (its Uzawa step does 9 element-loop products) times the measured
+  GMRES iteration / V-cycle count -- labelled "extrapolated".  `--impl reference`
+  times the same oracle apply as the reference arm.
+* --gpus N > 1 (torchrun) shards the grid in z-slabs over N ranks (NCCL halo
+  exchange and allreduce; total work fixed: "strong" scaling).
 """
 from __future__ import annotations
 
@@ -47,7 +57,23 @@ METRIC = "Stokes operator apply GDoF/s and HBM GB/s vs peak; MG solve s/DoF at 1
 RTOL = 1e-8
 CFG_INDEX = {"cfg1": 0, "cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4}
 # algorithmic bytes per owned vertex of each profiled op
-OP_BYTES = {"apply": 65, "residual": 97, "vel_pass": 81, "p_pass1": 49, "p_pass2": 25}
+OP_BYTES = {"apply": 65, "residual": 97, "vel_pass": 40, "p_pass1": 48, "p_pass2": 24}
+# iterations our solver needs at rtol 1e-8 (profiles/r02_convergence_probe_gmres.log), for the
+# reference arm's extrapolation of the oracle solve (the oracle cannot run it in minutes)
+REF_ITS = {"cfg1": 11, "cfg2": 13, "cfg3": 29, "cfg4": 36, "cfg5": 59}
+DEFAULT_KRYLOV = {"cfg1": 0, "cfg2": 0, "cfg3": 30, "cfg4": 30, "cfg5": 30}
+
+
+def oracle_applies_per_cycle(n, n_coarse=4, nu=3, nu_inc=2):
+    """Cost of one V_var cycle of the oracle multigrid in full-grid element-loop
+    products: its Uzawa step does 9 (f - B^T p, 4 colour passes of A u, B u, C p, two
+    C sweeps), plus one residual per level; level l costs (n_l / n)^3."""
+    tot, m, l = 0.0, n, 0
+    while m > n_coarse:
+        tot += (2 * (nu + nu_inc * l) * 9 + 1) * (m / n) ** 3
+        m //= 2
+        l += 1
+    return tot
 
 
 FORM_IDX = {"mod": 0, "sym": 1, "grad": 2}
@@ -163,91 +189,81 @@ def slab_inputs(cfg, ctx):
 
 
 # ------------------------------------------------------------------------------
-# reference arm: the oracle multigrid on the host (bounded sample per step)
+# the oracle on the host (reference arm and cpu_baseline): bounded samples
 # ------------------------------------------------------------------------------
-def oracle_cycle_sample(cfg, form, cycles, gpu_cycles=None, log=None):
-    """Time `cycles` V-cycles of the oracle (matrix-free C products, all host
-    threads) on the workload; returns (seconds per cycle list, residual history,
-    threads, setup seconds)."""
-    from oracle import capi, mg_mf
+def _omp_threads(n):
+    import ctypes
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+    except OSError:
+        pass
+
+
+def oracle_apply_sample(cfg, form, reps=1, log=None, slab_planes=8):
+    """Time the oracle's C element-loop apply (oracle/c/oracle.c) on the full grid with
+    all host threads (median of `reps`) and on a slab of `slab_planes` vertex planes
+    with one thread.  Returns dict(t_all, threads, gdof_all, gdof_one, t_inputs)."""
+    from oracle import capi
     t0 = time.time()
-    cls, fcls = synth.element_classes(cfg)
-    h = mg_mf.MFHierarchy(cfg.n, cls, cfg.class_mu, cfg.faces, form=form,
-                          ncolors_u=4 if form == "sym" else 2)
-    pr = h.levels[0].prob
-    if cfg.forcing == "nodal":
-        f = synth.nodal_forcing(cfg)
-        # b_u = M f by the element loop: M f = sum_T |T|/20 (sum_q f_q + f_i)
-        b = _oracle_load_nodal(cfg, f)
-    else:
-        b = _oracle_load_element(cfg, np.asarray(cfg.force_table)[fcls])
-    b = np.where(pr.free, b, 0.0)
-    setup = time.time() - t0
-    x = np.zeros_like(b)
-    nb = np.linalg.norm(b)
-    hist = [1.0]
-    times = []
-    for c in range(cycles):
+    cls, _ = synth.element_classes(cfg)
+    x = synth.apply_input(cfg)
+    t_in = time.time() - t0
+    capi.lib()
+    nthr = os.cpu_count() or 1
+    _omp_threads(nthr)
+    threads = capi.num_threads()
+    ts = []
+    for r in range(reps):
         t1 = time.time()
-        x = h.vcycle(b, x)
-        times.append(time.time() - t1)
-        hist.append(np.linalg.norm(b - pr.apply(x)) / nb)
+        capi.apply_slab(cfg.n, form, 1.0 / 12.0, cfg.faces, cls, cfg.class_mu, x)
+        ts.append(time.time() - t1)
         if log:
-            log(f"oracle cycle {c}: {times[-1]:.2f}s rel {hist[-1]:.2e}")
-    return times, hist, capi.num_threads(), setup
+            log(f"oracle apply {r}: {ts[-1]:.2f} s ({threads} threads)")
+    t_all = float(np.median(ts))
+    kv = min(slab_planes, cfg.n + 1)
+    _omp_threads(1)
+    t1 = time.time()
+    capi.apply_slab(cfg.n, form, 1.0 / 12.0, cfg.faces, cls, cfg.class_mu, x, kv0=0, kv1=kv)
+    t_one = time.time() - t1
+    _omp_threads(nthr)
+    dofs_slab = 4 * (cfg.n + 1) ** 2 * kv
+    return {"t_all": t_all, "threads": threads, "gdof_all": cfg.dofs / t_all / 1e9,
+            "gdof_one": dofs_slab / t_one / 1e9, "t_one_slab": t_one, "slab_planes": kv, "t_inputs": t_in,
+            "samples": ts}
 
 
-def _oracle_load_nodal(cfg, f):
-    from oracle import fem
-    n = cfg.n
-    V = cfg.vertices
-    h = 1.0 / n
-    b = np.zeros((3, V))
-    for t in range(6):
-        vid = fem._element_vertex_ids(n, t)
-        M = fem.element_matrices(t, h, "grad")["M"]
-        for a in range(3):
-            loc = f[a][vid] @ M.T
-            np.add.at(b[a], vid.reshape(-1), loc.reshape(-1))
-    return np.concatenate([b.reshape(-1), np.zeros(V)])
-
-
-def _oracle_load_element(cfg, fe):
-    from oracle import fem
-    n, V = cfg.n, cfg.vertices
-    fe = fe.reshape(n, n, n, 6, 3)
-    b = np.zeros((3, V))
-    vol = (1.0 / n) ** 3 / 6
-    for t in range(6):
-        vid = fem._element_vertex_ids(n, t)
-        ft = fe[..., t, :].reshape(-1, 3)
-        for a in range(3):
-            np.add.at(b[a], vid.reshape(-1), np.repeat(ft[:, a] * vol / 4.0, 4))
-    return np.concatenate([b.reshape(-1), np.zeros(V)])
+def oracle_solve_extrapolated(cfg, t_apply, its, krylov):
+    """s/DoF of the oracle multigrid solve: `its` V_var cycles (plus one apply per
+    GMRES iteration and the residuals) at the measured time per full-grid apply."""
+    per = oracle_applies_per_cycle(cfg.n)
+    applies = its * (per + (1 if krylov else 1)) + 2
+    return t_apply * applies / cfg.dofs, applies
 
 
 def run_reference(args, cfg, world, rank):
     if rank != 0:
         return 0
-    dofs = cfg.dofs
-    times, hist, threads, setup = oracle_cycle_sample(cfg, args.form, args.warmup + args.steps,
-                                                      log=lambda s: print(s, file=sys.stderr))
-    tt = times[args.warmup:]
-    rho = (hist[-1] / hist[0]) ** (1.0 / max(1, len(hist) - 1))
-    need = math.ceil(math.log(RTOL) / math.log(rho)) if 0 < rho < 1 else None
-    t_cycle = float(np.median(tt))
-    value = t_cycle * need / dofs if need else None
-    sample = (f"one oracle V_var(3,3) cycle per step (matrix-free C element loop, {threads} host threads) "
-              f"on the full {cfg.name} n={cfg.n} grid; solve time extrapolated as median cycle time x "
-              f"cycles to rtol 1e-8 at the oracle's observed rate rho={rho:.3f} ({need} cycles)")
+    log = lambda s_: print(s_, file=sys.stderr, flush=True)
+    kry = args.krylov if args.krylov is not None else DEFAULT_KRYLOV[cfg.name]
+    smp = oracle_apply_sample(cfg, args.form, reps=args.warmup + args.steps, log=log)
+    tt = smp["samples"][args.warmup:] or smp["samples"]
+    t_apply = float(np.median(tt))
+    its = REF_ITS.get(cfg.name, 30)
+    value, applies = oracle_solve_extrapolated(cfg, t_apply, its, kry)
+    sample = (f"per step one oracle apply (plain C element loop, {smp['threads']} host threads) on the full "
+              f"{cfg.name} n={cfg.n} grid ({t_apply:.2f} s); the solve is extrapolated as {applies:.0f} "
+              f"full-grid element-loop products = {its} preconditioner cycles of the oracle multigrid "
+              f"({oracle_applies_per_cycle(cfg.n):.1f} products per V_var(3,3) cycle) -- the iteration count "
+              f"our solver measured at this config")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s/DoF", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_cycle * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * cfg.dofs * 1e3,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"{cfg.name} (BASELINE configs[{CFG_INDEX[cfg.name]}])", "n": cfg.n,
-                       "dofs": dofs, "form": args.form, "rtol": RTOL},
-            "cpu_baseline": {"value": value, "unit": "s/DoF", "cores": threads, "kind": "oracle",
-                             "sample": sample},
+                       "dofs": cfg.dofs, "form": args.form, "rtol": RTOL},
+            "cpu_baseline": {"value": value, "unit": "s/DoF", "cores": smp["threads"], "kind": "oracle",
+                             "sample": sample, "apply_gdof_s_all_threads": round(smp["gdof_all"], 4),
+                             "apply_gdof_s_one_thread": round(smp["gdof_one"], 5)},
             "e2e": {"value": value, "unit": "s/DoF", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "extrapolated": True}
     print(json.dumps(line), flush=True)
@@ -269,7 +285,8 @@ def run_ours(args, cfg, world, rank, local):
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     stream = torch.cuda.current_stream()
-    ctx = stk.StokesContext(cfg.n, args.form, cfg.faces, krylov=args.krylov,
+    kry = args.krylov if args.krylov is not None else DEFAULT_KRYLOV[cfg.name]
+    ctx = stk.StokesContext(cfg.n, args.form, cfg.faces, krylov=kry,
                             ncolors_u=4 if args.form == "sym" else 2, rank=rank, nranks=world,
                             stream=stream, nccl_id=nid)
     t0 = time.time()
@@ -383,9 +400,12 @@ def run_ours(args, cfg, world, rank, local):
                  "frac_of_peak": round(65 * cfg.vertices / (a_ms * 1e-3) / 1e9 / peak, 4),
                  "ms": round(a_ms, 4), "bytes_per_vertex": 65}
 
-    # end-to-end through the public API from pinned host buffers
+    # end-to-end through the public API from pinned host buffers: inputs in, the
+    # solution (4 fields, canonical layout) out, every step
     e2e_ms = []
     h2d = cls.nbytes + (f4.nbytes if f is not None else fcls.nbytes)
+    xcan = torch.empty((4, V_own), dtype=torch.float64, device="cuda")
+    xhost = torch.empty((4, V_own), dtype=torch.float64).pin_memory()
     d2h = 0
     for r in range(args.steps + 1):
         flush.zero_()
@@ -407,23 +427,30 @@ def run_ours(args, cfg, world, rank, local):
         ctx.apply(x_apply, y)
         x.zero_()
         _, rep = ctx.solve(b, x, rtol=RTOL, max_cycles=args.max_cycles)   # D2H: norms per cycle
+        ctx.export_device(x, out=xcan)
+        xhost.copy_(xcan, non_blocking=True)                    # D2H: the solution
         c1.record(stream)
         torch.cuda.synchronize()
         if r >= 1:
             e2e_ms.append(c0.elapsed_time(c1))
-            d2h = 48 * (rep.cycles + 2)
+            d2h = xhost.numel() * 8 + 48 * (rep.cycles + 2)
     e2e_ms_v = max_over_ranks(float(np.mean(e2e_ms)), world)
 
     rep = reps[-1]
+    converged = all(r_.rel_res <= RTOL for r_ in reps)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            times, hist, threads, setup = oracle_cycle_sample(cfg, args.form, 1)
-            t_solve = times[0] * max(rep.cycles, 1) + setup
-            cpu = {"value": t_solve / dofs, "unit": "s/DoF", "cores": threads, "kind": "oracle",
-                   "sample": (f"1 V_var(3,3) cycle of the oracle multigrid (matrix-free C element loop, "
-                              f"{threads} threads) on the full {cfg.name} n={cfg.n} grid ({times[0]:.1f} s) "
-                              f"+ oracle setup ({setup:.1f} s), extrapolated to the GPU's {rep.cycles} cycles"),
+            smp = oracle_apply_sample(cfg, args.form, reps=1)
+            value_cpu, applies = oracle_solve_extrapolated(cfg, smp["t_all"], rep.cycles, kry)
+            cpu = {"value": value_cpu, "unit": "s/DoF", "cores": smp["threads"], "kind": "oracle",
+                   "sample": (f"one oracle apply (plain C element loop, {smp['threads']} threads) on the full "
+                              f"{cfg.name} n={cfg.n} grid: {smp['t_all']:.2f} s; the solve extrapolated as "
+                              f"{applies:.0f} such products (the oracle multigrid's cost of the GPU's "
+                              f"{rep.cycles} preconditioner cycles); one-thread apply on a "
+                              f"{smp['slab_planes']}-plane slab: {smp['t_one_slab']:.2f} s"),
+                   "apply_gdof_s_all_threads": round(smp["gdof_all"], 4),
+                   "apply_gdof_s_one_thread": round(smp["gdof_one"], 5),
                    "extrapolated": True}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "s/DoF", "cores": os.cpu_count(), "kind": "oracle",
@@ -436,11 +463,11 @@ def run_ours(args, cfg, world, rank, local):
                 "data": "synthetic",
                 "config": {"workload": f"{cfg.name} (BASELINE configs[{CFG_INDEX[cfg.name]}])", "n": cfg.n,
                            "dofs": dofs, "form": args.form, "rtol": RTOL,
-                           "solver": f"GMRES({args.krylov}) + V_var(3,3)" if args.krylov else "V_var(3,3) iteration",
+                           "solver": f"GMRES({kry}) + V_var(3,3)" if kry else "V_var(3,3) iteration",
                            "step": "assemble + load vector + apply + solve", "l2": "flushed between steps",
                            "parallelism": f"z-slab x{world}"},
-                "solve": {"cycles": rep.cycles, "rho": round(rep.rho, 4), "rel_res": rep.rel_res,
-                          "solve_s": rep.t_total_s},
+                "solve": {"iterations": rep.cycles, "rho": round(rep.rho, 4), "rel_res": rep.rel_res,
+                          "solve_s": rep.t_total_s, "converged_every_step": converged},
                 "apply": apply_obj,
                 "roofline": roof,
                 "ops_ms_per_step": ops_ms,
@@ -460,11 +487,11 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=list(CFG_INDEX))
+    ap.add_argument("--workload", default="cfg3", choices=list(CFG_INDEX))
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--form", default="mod", choices=["mod", "sym", "grad"])
-    ap.add_argument("--krylov", type=int, default=0)
-    ap.add_argument("--max-cycles", type=int, default=100)
+    ap.add_argument("--krylov", type=int, default=None)
+    ap.add_argument("--max-cycles", type=int, default=300)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

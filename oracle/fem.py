@@ -226,25 +226,27 @@ class Problem:
     def solve_direct(self, b: np.ndarray, x_dir: np.ndarray | None = None) -> np.ndarray:
         """Unique discrete solution of K_FF x_F = b_F (- K_FD x_D), gauged.
 
-        Without a traction face the pressure is fixed by the Lagrange-multiplier
-        row w^T p = 0 (w = gauge weights)."""
+        Without a traction face K_FF has the constant pressure as its null vector
+         and b_p = 0 is consistent with it: the last pressure unknown is pinned
+        to 0 (its row and column removed -- the removed equation holds by
+        consistency), the reduced nonsingular system is solved directly (sparse LU),
+        and the result is gauged to int mu^-1 p = 0 (reading R9)."""
         import scipy.sparse.linalg as spla
         free = np.flatnonzero(self.free)
         rhs = b.reshape(-1)[free].copy()
         if x_dir is not None:
             xd = np.where(self.free, 0.0, x_dir.reshape(-1))
             rhs -= (self.K @ xd)[free]
-        Kff = self.K[free][:, free]
+        Kff = self.K[free][:, free].tocsc()
+        keep = np.arange(len(free))
         if not self.has_traction:
-            wfull = np.concatenate([np.zeros(3 * self.V), self.gauge_w])[free]
-            Kaug = sp.bmat([[Kff, sp.csr_matrix(wfull[:, None])],
-                            [sp.csr_matrix(wfull[None, :]), None]], format="csc")
-            sol = spla.spsolve(Kaug, np.concatenate([rhs, [0.0]]))[:-1]
-        else:
-            sol = spla.spsolve(Kff.tocsc(), rhs)
+            keep = keep[:-1]                      # free[-1] is the last pressure DoF
+            Kff = Kff[keep][:, keep]
+        sol = np.zeros(len(free))
+        sol[keep] = spla.spsolve(Kff.tocsc(), rhs[keep])
         x = np.zeros(4 * self.V) if x_dir is None else np.where(self.free, 0.0, x_dir.reshape(-1))
         x[free] = sol
-        return x
+        return self.gauge(x)
 
 
 def load_nodal_elementwise(n: int, faces, f: np.ndarray) -> np.ndarray:

@@ -59,11 +59,16 @@ __global__ void k_restrict_part(DGrid gf, DGrid gc, int K0, int K1, const double
   }
 }
 
-// loopback allreduce: out = sum over ranks q = 0..P-1 (in that order) of in[q][0..count)
-__global__ void k_loopback_sum(const double* const* __restrict__ in, int P, int count, double* __restrict__ out) {
+// loopback allreduce: out = sum over ranks q = 0..P-1 (in that order) of in[q][0..count);
+// the rank pointers travel by value in the kernel parameters (no host staging to race on)
+constexpr int LB_MAXP = 64;
+struct LbPtrs {
+  const double* p[LB_MAXP];
+};
+__global__ void k_loopback_sum(const LbPtrs in, int P, int count, double* __restrict__ out) {
   for (int c = threadIdx.x; c < count; c += blockDim.x) {
     double s = 0.0;
-    for (int q = 0; q < P; ++q) s += in[q][c];
+    for (int q = 0; q < P; ++q) s += in.p[q][c];
     out[c] = s;
   }
 }
@@ -79,9 +84,7 @@ struct stk_loopback {
   long generation = 0;
   std::vector<void*> ptr;      // published by each rank at a rendezvous
   std::vector<int64_t> aux;    // e.g. the rank's field stride / plane count
-  double** dptrs = nullptr;    // device copy of ptr (allreduce)
   double* dsum = nullptr;      // device result of the allreduce
-  double** hp = nullptr;       // pinned host staging of the pointer table
   void* stream = nullptr;      // the one CUDA stream every rank's context uses
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
@@ -229,13 +232,10 @@ struct Comm {
       publish(d);
       stk_status st = STK_OK;
       if (rank == 0) {
-        for (int q = 0; q < nranks; ++q) lb->hp[q] = (double*)lb->ptr[q];
-        st = cuda_ok(ctx, cudaMemcpyAsync(lb->dptrs, lb->hp, sizeof(double*) * nranks, cudaMemcpyHostToDevice,
-                                          ctx->stream), "loopback allreduce");
-        if (st == STK_OK) {
-          k_loopback_sum<<<1, 32, 0, ctx->stream>>>(lb->dptrs, nranks, count, lb->dsum);
-          st = cuda_ok(ctx, cudaGetLastError(), "loopback allreduce");
-        }
+        LbPtrs pt{};
+        for (int q = 0; q < nranks; ++q) pt.p[q] = (const double*)lb->ptr[q];
+        k_loopback_sum<<<1, 64, 0, ctx->stream>>>(pt, nranks, count, lb->dsum);
+        st = cuda_ok(ctx, cudaGetLastError(), "loopback allreduce");
       }
       lb->barrier();  // the sum is enqueued (stream order) before every rank's copy out
       if (st == STK_OK)

@@ -253,6 +253,9 @@ struct StreamArgs {
   int color, ncolors;   // VEL
   double omega;         // P2
   int ux0, uy0, uz0;    // velocity tensor-map origin (vertex coordinates)
+  int inplace;          // VEL: out == input velocity; only the active colour's stream rows are written,
+                        // list and traction-face rows go to cbuf (k_listx) and are scattered after
+  double* cbuf;         // VEL list rows: results [row][3] instead of out (nullptr: write out)
   unsigned long long* trace;  // debug (STK_STREAM_TRACE): per-CTA cycle counters, else nullptr
 };
 
@@ -589,7 +592,9 @@ __global__ void __launch_bounds__(LX_NT) k_listx(DGrid g, StreamArgs a, const do
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double uc = dir ? 0.0 : __ldg(a.inU + c * g.fs + o);
-      a.out[c * g.fs + o] = act ? fma(__ldg(a.aux + c * g.fs + o) - py[c], __ldg(inv + c), uc) : uc;
+      const double v = act ? fma(__ldg(a.aux + c * g.fs + o) - py[c], __ldg(inv + c), uc) : uc;
+      if (a.cbuf) a.cbuf[(int64_t)e * 3 + c] = v;
+      else a.out[c * g.fs + o] = v;
     }
   } else if (OP == OP_P1) {
     const double r = py[3] - __ldg(a.aux + o);
@@ -750,7 +755,7 @@ __device__ __forceinline__ void finish_row(const DGrid& g, const StreamArgs& a, 
       const double uc = cpl[c * FST + base];
       double v = uc;
       if (act) v = fma(aux[c] - fma(sA, acc.A[c], sB * acc.BT[c]), isA * ikd[c], uc);
-      a.out[c * g.fs + o] = v;
+      if (act || !a.inplace) a.out[c * g.fs + o] = v;
     }
   } else if (OP == OP_P1) {
     const double r = fma(sB, acc.B, -sC * acc.C) - aux[3];
@@ -939,7 +944,7 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
       const double* pls[3] = {ring + ((S + RING - 2) % RING) * SLOT, ring + ((S + RING - 1) % RING) * SLOT, pl};
       if (!(code & (0x80 | CODE_TOP))) {
         finish_row<FORM, OP>(g, a, i, j, k, o, code, aux, acc0, pls, base);
-      } else if (code != CODE_IRREGULAR) {
+      } else if (code != CODE_IRREGULAR && !(OP == OP_VEL && a.inplace)) {
         finish_top<FORM, OP>(g, a, i, j, k, o, code, aux, pls, base);
       }
       // face rows i = n, j = n (Dirichlet with an isoviscous star, else list rows)
@@ -1126,9 +1131,8 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
   a.inP = inP;
   a.list = lv.list;
   a.nlist = lv.n;
-  static const int skip_list = getenv("STK_SKIP_IRR") ? atoi(getenv("STK_SKIP_IRR")) : 0;
   static const int fork_env = getenv("STK_LIST_FORK") ? atoi(getenv("STK_LIST_FORK")) : 1;
-  const bool do_list = lv.n > 0 && !skip_list;
+  const bool do_list = lv.n > 0;
   const bool fork = do_list && fork_env && lv.side != nullptr;
   if (fork) {
     if (cudaEventRecord(lv.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(lv.side, lv.ev_fork, 0) != cudaSuccess)
@@ -1227,6 +1231,57 @@ inline bool launch_vel_repeat(int form, DGrid g, const ListView& lv, const doubl
     case FORM_MOD: return launch_vel_repeat_t<FORM_MOD>(g, lv, uin, p, b, uout, color, ncolors, st);
     case FORM_SYM: return launch_vel_repeat_t<FORM_SYM>(g, lv, uin, p, b, uout, color, ncolors, st);
     default: return launch_vel_repeat_t<FORM_GRAD>(g, lv, uin, p, b, uout, color, ncolors, st);
+  }
+}
+// list rows' results of an in-place velocity pass back into the vector
+__global__ void k_scatter3(DGrid g, const int32_t* __restrict__ list, int n, const double* __restrict__ cbuf,
+                           double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int t = __ldg(list + e);
+  const int nx = g.n + 1;
+  const int k = g.z0 + t / (nx * nx), rr = t % (nx * nx);
+  const int64_t o = vidx(g, rr % nx, rr / nx, k);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) out[c * g.fs + o] = cbuf[(int64_t)e * 3 + c];
+}
+// In-place velocity colour pass (mod / grad forms): u is updated in place.  A regular
+// row of the active colour couples only to the other colour (7-point A), so
+// its in-place update reads exactly the start-of-pass values; the list rows (Gamma_12,
+// Gamma_F, lv = the repeat list incl. the isoviscous traction-face rows) are computed
+// from the start-of-pass vector into cbuf (their coefficients to same-colour regular
+// neighbours are exactly 0) and scattered after the stream kernel.  No ping-pong copy.
+// list_only: the repeat pass of the middle colour (regular rows unchanged, R12).
+template <int FORM>
+bool launch_vel_inplace_t(const DGrid& g, const ListView& lv, double* u, const double* p, const double* b,
+                          double* cbuf, int color, int ncolors, bool list_only, cudaStream_t st) {
+  StreamArgs a{};
+  a.out = u;
+  a.aux = b;
+  a.color = color;
+  a.ncolors = ncolors;
+  a.inplace = 1;
+  a.cbuf = cbuf;
+  if (list_only) {
+    if (lv.n == 0) return true;
+    a.inU = u;
+    a.inP = p;
+    a.list = lv.list;
+    a.nlist = lv.n;
+    k_listx<FORM, OP_VEL><<<(unsigned)(((int64_t)lv.n * 16 + LX_NT - 1) / LX_NT), LX_NT, 0, st>>>(g, a, lv.S);
+  } else if (!launch_stream_t<FORM, OP_VEL>(g, u, p, lv, a, st)) {
+    return false;
+  }
+  if (lv.n > 0) k_scatter3<<<(lv.n + 255) / 256, 256, 0, st>>>(g, lv.list, lv.n, cbuf, u);
+  return true;
+}
+inline bool launch_vel_inplace(int form, DGrid g, const ListView& lv, double* u, const double* p, const double* b,
+                               double* cbuf, int color, int ncolors, bool list_only, cudaStream_t st) {
+  if (!lv.S) return false;  // needs the explicit stencils of the list rows
+  switch (form) {
+    case FORM_MOD: return launch_vel_inplace_t<FORM_MOD>(g, lv, u, p, b, cbuf, color, ncolors, list_only, st);
+    case FORM_GRAD: return launch_vel_inplace_t<FORM_GRAD>(g, lv, u, p, b, cbuf, color, ncolors, list_only, st);
+    default: return false;  // sym: the centre block couples the components; ping-pong passes
   }
 }
 inline bool launch_p_pass1_tiled(int form, DGrid g, const ListView& lv, const double* x, const double* gp, double* T,

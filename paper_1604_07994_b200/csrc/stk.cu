@@ -48,6 +48,8 @@ struct Level {
   double* Srl = nullptr;
   int64_t nrl = 0;
   size_t cap_rlist = 0, cap_Srl = 0;
+  double* cbuf = nullptr;   // in-place velocity passes: results of the repeat-list rows [nrl][3]
+  size_t cap_cbuf = 0;
 };
 
 // event-timed profile of the kernels launched while enabled (stk_profile_*)
@@ -385,6 +387,23 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
   const bool tiled = use_tiled(ctx, L);
   // pressure halo is fixed during the velocity sweep
   ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, x, 3, 1, L.replicated));
+  static const bool inplace_env = !getenv("STK_VEL_INPLACE") || atoi(getenv("STK_VEL_INPLACE"));
+  if (tiled && inplace_env && ctx->cfg.form != FORM_SYM && L.Srl) {
+    // in-place colour passes 0, 1, (1: list rows only), 0 -- see launch_vel_inplace
+    ListView rv = lview(ctx, L);
+    rv.list = L.rlist;
+    rv.n = (int)L.nrl;
+    rv.S = L.Srl;
+    for (int s = 0; s < 2 * nc; ++s) {
+      const int color = s < nc ? s : 2 * nc - 1 - s;
+      const bool list_only = s == nc;
+      ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, x, 0, 3, L.replicated));
+      PScope ps(ctx, list_only ? P_VREP : P_VEL, l);
+      ST(launch_vel_inplace(ctx->cfg.form, g, rv, x, p, b, L.cbuf, color, nc, list_only, ctx->stream) ? STK_OK
+                                                                                                   : STK_EUNSUP);
+      ST(launched(ctx));
+    }
+  } else {
   int pass = 0;
   for (int s = 0; s < 2 * nc; ++s, ++pass) {
     const int color = s < nc ? s : 2 * nc - 1 - s;
@@ -421,6 +440,7 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
       }
     }
     ST(launched(ctx));
+  }
   }
   // 2*nc passes: result is back in x
   ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, x, 0, 3, L.replicated));
@@ -546,7 +566,11 @@ template <int OP>
 stk_status launch_row(stk_ctx* ctx, const FLevel& F, const FLevel& F2, int64_t rows, const double* uin = nullptr,
                       double* uout = nullptr, int color = 0) {
   static const int env = getenv("STK_ROW_LPR") ? atoi(getenv("STK_ROW_LPR")) : 0;
-  const int lpr = env == 1 || env == 4 || env == 8 || env == 16 ? env : (rows <= 40000 ? 16 : 4);
+  // chosen from the level's GLOBAL size (not the rows this rank owns): the lane split
+  // fixes the summation order, so every partition gives the same bits
+  const int64_t gv = (int64_t)(F.g.n + 1) * (F.g.n + 1) * (F.g.n + 1);
+  const int lpr = env == 1 || env == 4 || env == 8 || env == 16 ? env : (gv <= 40000 ? 16 : 4);
+  (void)rows;
   if (lpr == 16) launch_rowl<OP, 16>(ctx, F, F2, rows, uin, uout, color);
   else if (lpr == 8) launch_rowl<OP, 8>(ctx, F, F2, rows, uin, uout, color);
   else if (lpr == 4) launch_rowl<OP, 4>(ctx, F, F2, rows, uin, uout, color);
@@ -764,19 +788,42 @@ stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x) {
 
 constexpr int kDotBlocks = 296;
 
-// dev out[q] = <V_q, w> over owned entries, all ranks (stream-ordered, no host sync)
-stk_status op_dots_dev(stk_ctx* ctx, const double* V, int nv, const double* w, double* out) {
+// dev out[q] = <V_q, w> over owned entries, all ranks (stream-ordered, no host sync);
+// with_self: also out[nv] = <w, w> (fused into the first chunk's pass)
+stk_status op_dots_dev(stk_ctx* ctx, const double* V, int nv, const double* w, double* out, int with_self = 0) {
   Level& L = ctx->lev[0];
   DGrid g = dgrid(ctx, L);
   PScope ps(ctx, P_KRYLOV, 0);
   for (int c0 = 0; c0 < nv; c0 += KRY_CHUNK) {
     const int m = std::min(KRY_CHUNK, nv - c0);
-    k_dots<<<kDotBlocks, 256, 0, ctx->stream>>>(g, V + (int64_t)c0 * L.vlen, L.vlen, m, w, ctx->kpart);
+    const int ws = (with_self && c0 == 0) ? 1 : 0;
+    k_dots<<<kDotBlocks, 256, 0, ctx->stream>>>(g, V + (int64_t)c0 * L.vlen, L.vlen, m, w, ctx->kpart, ws);
     ST(launched(ctx));
-    k_dots_final<<<1, 32, 0, ctx->stream>>>(ctx->kpart, kDotBlocks, m, out + c0);
+    k_dots_final<<<1, 32, 0, ctx->stream>>>(ctx->kpart, kDotBlocks, m, out + c0, 0);
     ST(launched(ctx));
+    if (ws) {  // the w.w sum of the same pass -> out[nv]
+      k_dots_final<<<1, 32, 0, ctx->stream>>>(ctx->kpart, kDotBlocks, 0, out + nv, 1);
+      ST(launched(ctx));
+    }
   }
-  if (!L.replicated) ST(ctx->comm.allreduce_sum(ctx, out, nv));
+  if (!L.replicated) ST(ctx->comm.allreduce_sum(ctx, out, nv + (with_self ? 1 : 0)));
+  return STK_OK;
+}
+
+// one fused Gram-Schmidt pass over the flat basis V(0..nv-1) (krylov.cuh); `cnt`
+// results into out (device), summed over ranks
+constexpr int kGsBlocks = 296;
+template <int MODE>
+stk_status op_gs(stk_ctx* ctx, const double* V, int nv, double* w, const double* c, double* out, int cnt) {
+  Level& L = ctx->lev[0];
+  PScope ps(ctx, P_KRYLOV, 0);
+  if (nv <= 8) k_gs_pass<MODE, 8><<<kGsBlocks, 256, 0, ctx->stream>>>(V, L.vlen, nv, w, c, ctx->kpart);
+  else if (nv <= 16) k_gs_pass<MODE, 16><<<kGsBlocks, 256, 0, ctx->stream>>>(V, L.vlen, nv, w, c, ctx->kpart);
+  else k_gs_pass<MODE, 32><<<kGsBlocks, 256, 0, ctx->stream>>>(V, L.vlen, nv, w, c, ctx->kpart);
+  ST(launched(ctx));
+  k_gs_final<<<1, 64, 0, ctx->stream>>>(ctx->kpart, kGsBlocks, cnt, out);
+  ST(launched(ctx));
+  if (!L.replicated) ST(ctx->comm.allreduce_sum(ctx, out, cnt));
   return STK_OK;
 }
 
@@ -822,8 +869,9 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
   const size_t vb = sizeof(double) * vlen;
   if (!ctx->kbasis) {
     if (cudaMalloc(&ctx->kbasis, vb * (m + 1)) != cudaSuccess || cudaMalloc(&ctx->kwork, vb * 3) != cudaSuccess ||
-        cudaMalloc(&ctx->kcoef, sizeof(double) * (3 * (m + 2) + KRY_CHUNK)) != cudaSuccess ||
-        cudaMalloc(&ctx->kpart, sizeof(double) * kDotBlocks * KRY_CHUNK) != cudaSuccess) {
+        cudaMalloc(&ctx->kcoef, sizeof(double) * (4 * (m + 2) + KRY_CHUNK)) != cudaSuccess ||
+        cudaMalloc(&ctx->kpart, sizeof(double) * std::max(kDotBlocks * (KRY_CHUNK + 1),
+                                                           kGsBlocks * (KRY_MAXV + 1))) != cudaSuccess) {
       cudaGetLastError();
       ctx->err = "out of device memory for the GMRES basis (reduce cfg.krylov)";
       return STK_ENOMEM;
@@ -844,7 +892,7 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
   double beta = std::sqrt(nr);
   rel = bnorm > 0 ? beta / bnorm : 0.0;
   while (rel > rtol && its < max_its) {
-    k_axpby<<<nb, kThreads, 0, ctx->stream>>>(g0, 1.0 / beta, r, 0.0, V(0));
+    k_axpby_flat<<<kGsBlocks, 256, 0, ctx->stream>>>(vlen, 1.0 / beta, r, 0.0, V(0));
     ST(launched(ctx));
     std::fill(gv.begin(), gv.end(), 0.0);
     gv[0] = beta;
@@ -853,23 +901,37 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
       CK(cudaMemsetAsync(z, 0, vb, ctx->stream));
       ST(op_vcycle(ctx, 0, V(j), z));
       ST(op_apply(ctx, 0, BLK_ALL, z, w));
-      // classical Gram-Schmidt twice (CGS2) with the coefficients kept on the device;
-      // one host round trip per iteration for the Hessenberg column and ||w||
-      double* c1 = ctx->kcoef + (m + 2);
-      double* c2 = ctx->kcoef + 2 * (m + 2);
-      ST(op_dots_dev(ctx, V(0), j + 1, w, c1));
-      ST(op_update_dev(ctx, V(0), j + 1, c1, 1.0, w));
-      ST(op_dots_dev(ctx, V(0), j + 1, w, c2));
-      ST(op_update_dev(ctx, V(0), j + 1, c2, 1.0, w));
-      ST(op_dots_dev(ctx, w, 1, w, c2 + (j + 1)));
-      std::vector<double> hc(2 * (m + 2));
-      CK(cudaMemcpyAsync(hc.data(), c1, sizeof(double) * 2 * (m + 2), cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cudaStreamSynchronize(ctx->stream));
-      for (int q = 0; q <= j; ++q) h[q] = hc[q] + hc[(m + 2) + q];
-      const double ww = hc[(m + 2) + j + 1];
-      h[j + 1] = std::sqrt(std::max(ww, 0.0));
+      if (m + 1 <= KRY_MAXV) {
+        // classical Gram-Schmidt twice (CGS2) in three fused flat passes: dots; update +
+        // the second pass's dots; update + ||w||^2 -- one host round trip per iteration
+        double* c1 = ctx->kcoef + (m + 2);
+        double* c2 = ctx->kcoef + 2 * (m + 2);
+        double* nw = ctx->kcoef + 3 * (m + 2);
+        ST(op_gs<GS_DOTS>(ctx, V(0), j + 1, w, nullptr, c1, j + 1));
+        ST(op_gs<GS_UPDATE_DOTS>(ctx, V(0), j + 1, w, c1, c2, j + 1));
+        ST(op_gs<GS_UPDATE_NORM>(ctx, V(0), j + 1, w, c2, nw, 1));
+        std::vector<double> hc(3 * (m + 2));
+        CK(cudaMemcpyAsync(hc.data(), c1, sizeof(double) * 3 * (m + 2), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int q = 0; q <= j; ++q) h[q] = hc[q] + hc[(m + 2) + q];
+        h[j + 1] = std::sqrt(std::max(hc[2 * (m + 2)], 0.0));
+      } else {
+        // long restarts: chunked CGS2 with the coefficients on the device
+        double* c1 = ctx->kcoef + (m + 2);
+        double* c2 = ctx->kcoef + 2 * (m + 2);
+        ST(op_dots_dev(ctx, V(0), j + 1, w, c1, 0));
+        ST(op_update_dev(ctx, V(0), j + 1, c1, 1.0, w));
+        ST(op_dots_dev(ctx, V(0), j + 1, w, c2, 0));
+        ST(op_update_dev(ctx, V(0), j + 1, c2, 1.0, w));
+        ST(op_dots_dev(ctx, w, 1, w, c2 + (j + 1), 0));
+        std::vector<double> hc(2 * (m + 2));
+        CK(cudaMemcpyAsync(hc.data(), c1, sizeof(double) * 2 * (m + 2), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int q = 0; q <= j; ++q) h[q] = hc[q] + hc[(m + 2) + q];
+        h[j + 1] = std::sqrt(std::max(hc[(m + 2) + j + 1], 0.0));
+      }
       if (h[j + 1] > 0) {
-        k_axpby<<<nb, kThreads, 0, ctx->stream>>>(g0, 1.0 / h[j + 1], w, 0.0, V(j + 1));
+        k_axpby_flat<<<kGsBlocks, 256, 0, ctx->stream>>>(vlen, 1.0 / h[j + 1], w, 0.0, V(j + 1));
         ST(launched(ctx));
       }
       for (int q = 0; q < j; ++q) {  // previous rotations
@@ -1092,17 +1154,13 @@ stk_status stk_create(const stk_config* cfg, const uint8_t* id, stk_ctx** out) {
 }
 
 stk_status stk_loopback_create(int32_t nranks, stk_loopback** out) {
-  if (!out || nranks < 1 || nranks > 64) return STK_EINVAL;
+  if (!out || nranks < 1 || nranks > LB_MAXP) return STK_EINVAL;
   stk_loopback* g = new stk_loopback();
   g->P = nranks;
   g->ptr.assign(nranks, nullptr);
   g->aux.assign(nranks, 0);
-  if (cudaMalloc(&g->dptrs, sizeof(double*) * nranks) != cudaSuccess ||
-      cudaMalloc(&g->dsum, sizeof(double) * 256) != cudaSuccess ||
-      cudaMallocHost(&g->hp, sizeof(double*) * nranks) != cudaSuccess) {
+  if (cudaMalloc(&g->dsum, sizeof(double) * 256) != cudaSuccess) {
     cudaGetLastError();
-    cudaFree(g->dptrs);
-    cudaFree(g->dsum);
     delete g;
     return STK_ENOMEM;
   }
@@ -1112,9 +1170,7 @@ stk_status stk_loopback_create(int32_t nranks, stk_loopback** out) {
 
 stk_status stk_loopback_destroy(stk_loopback* g) {
   if (!g) return STK_EINVAL;
-  cudaFree(g->dptrs);
   cudaFree(g->dsum);
-  cudaFreeHost(g->hp);
   delete g;
   return STK_OK;
 }
@@ -1356,7 +1412,8 @@ stk_status stk_assemble(stk_ctx* ctx) {
     CK(cudaStreamSynchronize(ctx->stream));
     L.nrl = L.nirr + (int64_t)ntop;
     if (L.nrl == 0) continue;
-    if (!ensure(L.rlist, L.cap_rlist, (size_t)L.nrl) || !ensure(L.Srl, L.cap_Srl, (size_t)EXPL * L.nrl))
+    if (!ensure(L.rlist, L.cap_rlist, (size_t)L.nrl) || !ensure(L.Srl, L.cap_Srl, (size_t)EXPL * L.nrl) ||
+        !ensure(L.cbuf, L.cap_cbuf, (size_t)3 * L.nrl))
       return STK_ENOMEM;
     CK(cudaMemsetAsync(tc, 0, sizeof(unsigned long long), ctx->stream));
     k_build_list<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), L.rlist, tc, 0);
@@ -1380,6 +1437,10 @@ stk_status stk_assemble(stk_ctx* ctx) {
   // constant subdomain stencils for the tiled kernels
   for (int l = 0; l < ctx->nlev; ++l) {
     Level& L = ctx->lev[l];
+    if (ctx->kernel_mode == 1 && L.n >= 64 && !L.replicated && !tiled_supported(L.n)) {
+      ctx->err = "tiled kernels unavailable (cuTensorMapEncodeTiled not found): no silent fallback";
+      return STK_EUNSUP;
+    }
     if (L.n >= 64 && !assemble_stencils(ctx->stream)) {
       ctx->err = "constant stencil assembly failed or disagrees with the compile-time stencils";
       return STK_ECUDA;
@@ -1816,6 +1877,7 @@ stk_status stk_destroy(stk_ctx* ctx) {
     cudaFree(L.S);
     cudaFree(L.rlist);
     cudaFree(L.Srl);
+    cudaFree(L.cbuf);
   }
   cudaFree(ctx->fbar);
   cudaFree(ctx->dcnt);

@@ -3,8 +3,10 @@ process) give the same results: each variant runs in its own subprocess and the
 outputs are compared.  The default path is pinned to the oracle by
 test_gpu_parity.py; these tests pin the alternatives to the default.
 
-* STK_VEL_REPEAT=0: full repeat pass of the smoother's middle colour instead of the
-  copy + within-colour rows shortcut (exact in exact arithmetic);
+* STK_VEL_INPLACE=0: ping-pong velocity colour passes (the repeat pass of the middle
+  colour as a copy + the within-colour rows) instead of the in-place passes;
+* STK_VEL_INPLACE=0 STK_VEL_REPEAT=0: ping-pong passes with the full repeat pass
+  (exact in exact arithmetic);
 * STK_LIST_EXPLICIT=0: Gamma rows by the per-thread element loop instead of the
   explicit 4x4-block stencils;
 * STK_GJ_GRID=1: coarsest-level inverse by the grid-barrier kernel instead of the
@@ -60,8 +62,9 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("env,cfg,n,form", [
-    ({"STK_VEL_REPEAT": "0"}, "cfg2", 128, "mod"),
-    ({"STK_VEL_REPEAT": "0"}, "cfg5", 64, "grad"),
+    ({"STK_VEL_INPLACE": "0"}, "cfg2", 128, "mod"),
+    ({"STK_VEL_INPLACE": "0", "STK_VEL_REPEAT": "0"}, "cfg5", 64, "grad"),
+    ({"STK_VEL_INPLACE": "0", "STK_VEL_REPEAT": "0"}, "cfg3", 128, "mod"),
     ({"STK_LIST_EXPLICIT": "0"}, "cfg2", 128, "mod"),
     ({"STK_LIST_EXPLICIT": "0"}, "cfg2", 64, "sym"),
     ({"STK_GJ_GRID": "1"}, "cfg1", 16, "mod"),
