@@ -57,7 +57,7 @@ METRIC = "Stokes operator apply GDoF/s and HBM GB/s vs peak; MG solve s/DoF at 1
 RTOL = 1e-8
 CFG_INDEX = {"cfg1": 0, "cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4}
 # algorithmic bytes per owned vertex of each profiled op
-OP_BYTES = {"apply": 65, "residual": 97, "vel_pass": 40, "p_pass1": 48, "p_pass2": 24}
+OP_BYTES = {"apply": 65, "residual": 97, "vel_pass": 40, "p_pass1": 48, "p_pass2": 24, "fwd_sweep": 80}
 # iterations our solver needs at rtol 1e-8 (profiles/r02_convergence_probe_gmres.log), for the
 # reference arm's extrapolation of the oracle solve (the oracle cannot run it in minutes)
 REF_ITS = {"cfg1": 11, "cfg2": 13, "cfg3": 29, "cfg4": 36, "cfg5": 59}
@@ -372,7 +372,8 @@ def run_ours(args, cfg, world, rank, local):
         if n0 > 0:
             bytes_launch = OP_BYTES[dom] * V_own
             achieved = bytes_launch / (ms0 / n0 * 1e-3) / 1e9
-            kname = f"k_stream<{FORM_IDX[args.form]}, {OP_IDX[dom]}>"
+            kname = (f"k_fsweep<{FORM_IDX[args.form]}>" if dom == "fwd_sweep"
+                     else f"k_stream<{FORM_IDX[args.form]}, {OP_IDX[dom]}>")
             roof = {"bound": "hbm", "kernel": f"{kname} ({dom}, level 0)", "achieved": round(achieved, 1),
                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                     "traffic": ncu_traffic(kname), "traffic_source": "profiles/ncu_traffic.json (ncu --set full, "

@@ -228,7 +228,8 @@ int64_t stk_launch_count(const stk_ctx* ctx);
  * one op (0 apply, 1 residual, 2 velocity colour pass, 3 pressure pass 1,
  * 4 pressure pass 2, 5 restriction, 6 prolongation, 7 coarse solve,
  * 8 reductions, 9 Krylov vector ops, 10 coarse-level graph, 11 fused
- * coarse V-cycle kernel, 12 repeat pass of the smoother's middle colour) on one level
+ * coarse V-cycle kernel, 12 list-row passes of the smoother (repeat pass / list rows of
+ * the fused sweep), 13 fused forward velocity sweep (both colours)) on one level
  * (-1 = all); synchronises.  STK_EINVAL for on outside 0..2. */
 stk_status stk_profile_enable(stk_ctx* ctx, int32_t on);
 stk_status stk_profile_reset(stk_ctx* ctx);

@@ -284,7 +284,7 @@ class StokesContext:
         return _lib.stk_launch_count(self.h)
 
     PROFILE_OPS = ("apply", "residual", "vel_pass", "p_pass1", "p_pass2", "restrict", "prolong",
-                   "coarse", "reduce", "krylov", "coarse_graph", "fused", "vel_repeat")
+                   "coarse", "reduce", "krylov", "coarse_graph", "fused", "vel_repeat", "fwd_sweep")
 
     def profile(self, on=True):
         """Event-time every launch: True/1 (the coarse-level CUDA graph timed as one

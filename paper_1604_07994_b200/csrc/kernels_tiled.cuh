@@ -1016,14 +1016,14 @@ inline PFN_encodeTiled encoder() {
 // 4-D map (x, y, z-plane, field) over vertices [x0, x1] x [y0, y1] x [z0v, z1v]
 // of a level vector `base` (field 0), box = one staged plane of one field.
 inline bool make_map(CUtensorMap* map, const double* base, const DGrid& g, int nfields, int x0, int x1, int y0,
-                     int y1, int z0v, int z1v) {
+                     int y1, int z0v, int z1v, unsigned bx = HX, unsigned by = HY) {
   PFN_encodeTiled enc = encoder();
   if (!enc) return false;
   const double* origin = base + vidx_host(g, x0, y0, z0v);
   cuuint64_t dims[4] = {(cuuint64_t)(x1 - x0 + 1), (cuuint64_t)(y1 - y0 + 1), (cuuint64_t)(z1v - z0v + 1),
                         (cuuint64_t)nfields};
   cuuint64_t strides[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.py * 8, (cuuint64_t)g.fs * 8};
-  cuuint32_t box[4] = {HX, HY, 1, 1};
+  cuuint32_t box[4] = {bx, by, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)origin, dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -15,6 +15,7 @@
 #include "kernels_generic.cuh"
 #include "kernels_tiled.cuh"
 #include "kernels_fused.cuh"
+#include "kernels_sweep.cuh"
 #include "krylov.cuh"
 
 using namespace stk;
@@ -54,7 +55,7 @@ struct Level {
 
 // event-timed profile of the kernels launched while enabled (stk_profile_*)
 enum { P_APPLY = 0, P_RESID, P_VEL, P_P1, P_P2, P_RESTRICT, P_PROLONG, P_COARSE, P_REDUCE, P_KRYLOV, P_CGRAPH, P_FUSED,
-       P_VREP, P_NOPS };
+       P_VREP, P_FSWEEP, P_NOPS };
 struct ProfRec {
   int op, level;
   cudaEvent_t e0, e1;
@@ -388,7 +389,42 @@ stk_status op_uzawa(stk_ctx* ctx, int l, double* x, const double* b) {
   // pressure halo is fixed during the velocity sweep
   ST(ctx->comm.halo(ctx, L.n, L.z0, L.nzl, L.py, L.fs, x, 3, 1, L.replicated));
   static const bool inplace_env = !getenv("STK_VEL_INPLACE") || atoi(getenv("STK_VEL_INPLACE"));
-  if (tiled && inplace_env && ctx->cfg.form != FORM_SYM && L.Srl) {
+  // the fused forward sweep (kernels_sweep.cuh) is exact and parity-tested, but measured
+  // slower than the in-place colour passes on B200 (cfg3 n = 256: 648 us vs 2 x 320 us plus
+  // un-overlapped list passes): opt-in with STK_FSWEEP=1
+  static const bool fsweep_env = getenv("STK_FSWEEP") && atoi(getenv("STK_FSWEEP"));
+  if (tiled && fsweep_env && ctx->cfg.form != FORM_SYM && nc == 2 && ctx->cfg.nranks == 1 && L.Srl &&
+      sweep_supported(g)) {
+    // symmetric sweep 0, 1, (1), 0 (R12) with the forward half fused into one pass
+    // (kernels_sweep.cuh): colour-0 list rows -> k_fsweep (x -> tmp) -> colour-1 list rows
+    // -> repeat of the colour-1 list rows -> colour-0 pass (tmp -> x)
+    ListView rv = lview(ctx, L);
+    rv.list = L.rlist;
+    rv.n = (int)L.nrl;
+    rv.S = L.Srl;
+    {
+      PScope ps(ctx, P_VREP, l);
+      ST(launch_vel_inplace(ctx->cfg.form, g, rv, x, p, b, L.cbuf, 0, nc, true, ctx->stream) ? STK_OK : STK_EUNSUP);
+      ST(launched(ctx));
+    }
+    {
+      PScope ps(ctx, P_FSWEEP, l);
+      ST(launch_fsweep(ctx->cfg.form, g, x, b, tmp, ctx->stream) ? STK_OK : STK_EUNSUP);
+      ST(launched(ctx));
+    }
+    {
+      PScope ps(ctx, P_VREP, l);
+      ST(launch_vel_inplace(ctx->cfg.form, g, rv, tmp, p, b, L.cbuf, 1, nc, true, ctx->stream) ? STK_OK : STK_EUNSUP);
+      ST(launch_vel_inplace(ctx->cfg.form, g, rv, tmp, p, b, L.cbuf, 1, nc, true, ctx->stream) ? STK_OK : STK_EUNSUP);
+      ST(launched(ctx));
+    }
+    {
+      PScope ps(ctx, P_VEL, l);
+      ST(launch_vel_pass_tiled(ctx->cfg.form, g, lview(ctx, L), tmp, p, b, x, 0, nc, ctx->stream) ? STK_OK
+                                                                                               : STK_EUNSUP);
+      ST(launched(ctx));
+    }
+  } else if (tiled && inplace_env && ctx->cfg.form != FORM_SYM && L.Srl) {
     // in-place colour passes 0, 1, (1: list rows only), 0 -- see launch_vel_inplace
     ListView rv = lview(ctx, L);
     rv.list = L.rlist;

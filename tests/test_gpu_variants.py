@@ -10,7 +10,9 @@ test_gpu_parity.py; these tests pin the alternatives to the default.
 * STK_LIST_EXPLICIT=0: Gamma rows by the per-thread element loop instead of the
   explicit 4x4-block stencils;
 * STK_GJ_GRID=1: coarsest-level inverse by the grid-barrier kernel instead of the
-  8-CTA cluster kernel.
+  8-CTA cluster kernel;
+* STK_FSWEEP=1: the forward half of the symmetric velocity sweep as ONE fused kernel
+  (kernels_sweep.cuh: colour 0 on plane k+1, colour 1 on plane k; list rows around it).
 """
 import os
 import subprocess
@@ -68,6 +70,9 @@ def rel(a, b):
     ({"STK_LIST_EXPLICIT": "0"}, "cfg2", 128, "mod"),
     ({"STK_LIST_EXPLICIT": "0"}, "cfg2", 64, "sym"),
     ({"STK_GJ_GRID": "1"}, "cfg1", 16, "mod"),
+    ({"STK_FSWEEP": "1"}, "cfg2", 128, "mod"),
+    ({"STK_FSWEEP": "1"}, "cfg5", 64, "grad"),
+    ({"STK_FSWEEP": "1"}, "cfg3", 128, "mod"),
 ])
 def test_switch_matches_default(tmp_path, env, cfg, n, form):
     y_def = run_variant(tmp_path, {}, cfg, n, form, "default")
