@@ -55,13 +55,19 @@ import synth  # noqa: E402
 
 METRIC = "Stokes operator apply GDoF/s and HBM GB/s vs peak; MG solve s/DoF at 1/2/4/8 GPUs"
 RTOL = 1e-8
-CFG_INDEX = {"cfg1": 0, "cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4}
+CFG_INDEX = {"cfg1": 0, "cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4, "cols": None}
 # algorithmic bytes per owned vertex of each profiled op
 OP_BYTES = {"apply": 65, "residual": 97, "vel_pass": 40, "p_pass1": 48, "p_pass2": 24, "fwd_sweep": 80}
 # iterations our solver needs at rtol 1e-8 (profiles/r02_convergence_probe_gmres.log), for the
 # reference arm's extrapolation of the oracle solve (the oracle cannot run it in minutes)
-REF_ITS = {"cfg1": 11, "cfg2": 13, "cfg3": 29, "cfg4": 36, "cfg5": 59}
-DEFAULT_KRYLOV = {"cfg1": 0, "cfg2": 0, "cfg3": 30, "cfg4": 30, "cfg5": 30}
+REF_ITS = {"cfg1": 11, "cfg2": 13, "cfg3": 29, "cfg4": 36, "cfg5": 59, "cols": 13}
+DEFAULT_KRYLOV = {"cfg1": 0, "cfg2": 0, "cfg3": 30, "cfg4": 30, "cfg5": 30, "cols": 0}
+
+
+def workload_name(name):
+    i = CFG_INDEX[name]
+    return (f"{name} (BASELINE configs[{i}])" if i is not None else
+            f"{name} (SURVEY NEXT-1: the paper's viscosity columns, free slip, P:772-774 / P:1307)")
 
 
 def oracle_applies_per_cycle(n, n_coarse=4, nu=3, nu_inc=2):
@@ -259,7 +265,7 @@ def run_reference(args, cfg, world, rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * cfg.dofs * 1e3,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"{cfg.name} (BASELINE configs[{CFG_INDEX[cfg.name]}])", "n": cfg.n,
+            "config": {"workload": workload_name(cfg.name), "n": cfg.n,
                        "dofs": cfg.dofs, "form": args.form, "rtol": RTOL},
             "cpu_baseline": {"value": value, "unit": "s/DoF", "cores": smp["threads"], "kind": "oracle",
                              "sample": sample, "apply_gdof_s_all_threads": round(smp["gdof_all"], 4),
@@ -304,7 +310,7 @@ def run_ours(args, cfg, world, rank, local):
     fcls_pin = torch.from_numpy(fcls).pin_memory()
     ctx.set_viscosity(cls, cfg.class_mu)
     ctx.assemble()
-    fvec = ctx.import_(f_pin.cuda())
+    fvec = ctx.import_(f_pin.cuda(), mask=False)
     x_apply = ctx.import_(torch.from_numpy(xin).cuda())
     fcls_dev = fcls_pin.cuda()
     y = ctx.new_vector()
@@ -418,7 +424,7 @@ def run_ours(args, cfg, world, rank, local):
         ctx.set_viscosity(cls_pin.numpy(), cfg.class_mu)      # H2D: element classes
         ctx.assemble()
         if cfg.forcing == "nodal":
-            fv = ctx.import_(f_pin.numpy(), out=fvec)           # H2D: forcing
+            fv = ctx.import_(f_pin.numpy(), out=fvec, mask=False)  # H2D: forcing
             st = stk.stk_load_vector(ctx.h, 0, fv.data_ptr(), None, 0, b.data_ptr())
         else:
             fcls_dev.copy_(fcls_pin, non_blocking=True)         # H2D: forcing classes
@@ -462,7 +468,7 @@ def run_ours(args, cfg, world, rank, local):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
                 "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": f"{cfg.name} (BASELINE configs[{CFG_INDEX[cfg.name]}])", "n": cfg.n,
+                "config": {"workload": workload_name(cfg.name), "n": cfg.n,
                            "dofs": dofs, "form": args.form, "rtol": RTOL,
                            "solver": f"GMRES({kry}) + V_var(3,3)" if kry else "V_var(3,3) iteration",
                            "step": "assemble + load vector + apply + solve", "l2": "flushed between steps",

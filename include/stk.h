@@ -64,9 +64,14 @@ typedef enum {
 /* viscous form of the A block: modified a_tr, strain a_sym,
  * gradient (mu grad u, grad v) */
 typedef enum { STK_FORM_MOD = 0, STK_FORM_SYM = 1, STK_FORM_GRAD = 2 } stk_form;
-/* faces x0,x1,y0,y1,z0,z1: homogeneous Dirichlet u = 0 or traction
- * free sigma n = 0; Dirichlet wins on shared edges/corners */
-typedef enum { STK_FACE_DIRICHLET0 = 0, STK_FACE_TRACTION = 1 } stk_face;
+/* faces x0,x1,y0,y1,z0,z1: homogeneous Dirichlet u = 0, traction free
+ * sigma n = 0, or free-slip u.n = 0, n x sigma n = 0 (the
+ * face-normal velocity component is eliminated, the tangential ones are free; every
+ * vertex of a free-slip face is an explicit-stencil row).  Dirichlet wins on shared
+ * edges/corners; a vertex on free-slip faces of several normals loses each normal.
+ * stk_create needs a Dirichlet face or free-slip faces of all three normals (Korn,
+ * P:109-111); without traction faces the pressure is fixed by the gauge. */
+typedef enum { STK_FACE_DIRICHLET0 = 0, STK_FACE_TRACTION = 1, STK_FACE_FREESLIP = 2 } stk_face;
 /* block mask for stk_apply: y_u = [A u] + [B^T p], y_p = [B u] - [C p] */
 enum { STK_BLK_A = 1, STK_BLK_BT = 2, STK_BLK_B = 4, STK_BLK_C = 8, STK_BLK_ALL = 15 };
 /* where a canonical (non-padded) array lives */
@@ -156,6 +161,25 @@ stk_status stk_import(stk_ctx* ctx, int32_t level, const double* canon, int32_t 
                       double* dev_vec);
 stk_status stk_export(stk_ctx* ctx, int32_t level, const double* dev_vec, double* canon,
                       int32_t where);
+/* Coarsest-level solver, taking effect at the next stk_assemble.  kind 0 (default): the
+ * exact solve of the A_tr coarse system by a dense inverse ("a direct coarse grid
+ * solver ... is not problematic").  kind 1: the paper's Krylov coarse solver:
+ * the strain form A_sym on the coarse level, the momentum right-hand side corrected to
+ * r1 + B^T M_L^-1 r2 (DESIGN R25: M_L = diag int phi/mu, the 1/mu-weighted lumped mass),
+ * and block-diagonal preconditioned MINRES from zero -- minres_its iterations (stopping
+ * early at gamma_{j+1} <= 1e-14 gamma_1, R24), velocity block cg_its steps of
+ * Jacobi-preconditioned CG on A_sym, pressure block M_L -- in one thread block
+ * (kernels_minres.cuh).  kind 1 needs the coarsest level held whole (nranks == 1 or a
+ * replicated level, else STK_EUNSUP at assembly) and supports n_coarse up to 16.
+ * STK_EINVAL for kind outside 0..1, minres_its < 1, cg_its < 0. */
+stk_status stk_set_coarse_solver(stk_ctx* ctx, int32_t kind, int32_t minres_its, int32_t cg_its);
+/* Set the eliminated velocity entries of a device level vector to 0 (all three on
+ * Dirichlet faces, the normal one on free-slip faces, P:97 / P:104-105).  Operator
+ * inputs (stk_apply, stk_residual, stk_smooth, stk_solve's x) must hold 0 there when a
+ * face is free-slip: the constant-stencil kernels read boundary planes as stored
+ * (Dirichlet planes are never read).  stk_import does not mask -- a nodal forcing f is
+ * imported whole, since its boundary values enter b = M f at interior rows. */
+stk_status stk_zero_eliminated(stk_ctx* ctx, int32_t level, double* dev_vec);
 
 /* Right-hand side b = (f_h, 0).  kind 0: nodal f given as a
  * device level vector (padded layout, fields 0..2 = f; halo planes are

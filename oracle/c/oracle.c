@@ -14,8 +14,10 @@
  * eimu[e] = the 1/mu_T weight of C (equal to 1/emu on the finest level; the
  * coarse-level means of reading R15 on coarse levels).
  * with g_i = grad(lambda_i) obtained by inverting the 4x4 vertex matrix.
- * Velocity DoFs on the closure of Dirichlet faces are ignored on input and
- * written as 0 on output.  No stencils, no blocking: a loop over elements.
+ * Eliminated velocity DoFs -- all three components on the closure of a
+ * Dirichlet face (face type 0), the face-normal component on a free-slip
+ * face (type 2, u.n = 0) -- are ignored on input and written as 0 on
+ * output.  No stencils, no blocking: a loop over elements.
  * OpenMP only splits cube layers into two parity phases (no write conflicts).
  */
 #include <math.h>
@@ -96,9 +98,16 @@ static void build_elements(double h, elem_t E[6]) {
   }
 }
 
-static inline int is_dirichlet(int n, const int32_t* faces, int i, int j, int k) {
-  return (faces[0] == 0 && i == 0) || (faces[1] == 0 && i == n) || (faces[2] == 0 && j == 0) ||
-         (faces[3] == 0 && j == n) || (faces[4] == 0 && k == 0) || (faces[5] == 0 && k == n);
+/* bit a set: velocity component a of vertex (i,j,k) is eliminated */
+static inline int elim_bits(int n, const int32_t* faces, int i, int j, int k) {
+  const int on[6] = {i == 0, i == n, j == 0, j == n, k == 0, k == n};
+  int m = 0;
+  for (int f = 0; f < 6; ++f) {
+    if (!on[f]) continue;
+    if (faces[f] == 0) m |= 7;
+    else if (faces[f] == 2) m |= 1 << (f / 2);
+  }
+  return m;
 }
 
 /* contribution of element (ci,cj,ck,t) to the rows of its local vertices; rows
@@ -113,9 +122,9 @@ static void element_apply(int n, int form, double delta, const int32_t* faces, c
   for (int m = 0; m < 4; ++m) {
     int i = ci + e->off[m][0], j = cj + e->off[m][1], k = ck + e->off[m][2];
     vk[m] = k;
-    dir[m] = is_dirichlet(n, faces, i, j, k);
+    dir[m] = elim_bits(n, faces, i, j, k);
     vid[m] = i + N1 * (j + N1 * (int64_t)k);
-    for (int a = 0; a < 3; ++a) xl[a * 4 + m] = dir[m] ? 0.0 : x[a * V + vid[m]];
+    for (int a = 0; a < 3; ++a) xl[a * 4 + m] = ((dir[m] >> a) & 1) ? 0.0 : x[a * V + vid[m]];
     xl[12 + m] = x[3 * V + vid[m]];
   }
   const double (*A)[12] = e->A[form];
@@ -134,7 +143,7 @@ static void element_apply(int n, int form, double delta, const int32_t* faces, c
   for (int m = 0; m < 4; ++m) {
     if (vk[m] < kv0 || vk[m] >= kv1) continue;
     for (int a = 0; a < 3; ++a)
-      if (!dir[m]) y[a * V + vid[m]] += yl[a * 4 + m];
+      if (!((dir[m] >> a) & 1)) y[a * V + vid[m]] += yl[a * 4 + m];
     y[3 * V + vid[m]] += yl[12 + m];
   }
 }
@@ -197,9 +206,9 @@ int ora_apply_rows(int n, int form, double delta, const int32_t* faces, const do
             int64_t vid[4];
             for (int q = 0; q < 4; ++q) {
               int ii = ci + e->off[q][0], jj = cj + e->off[q][1], kk = ck + e->off[q][2];
-              dir[q] = is_dirichlet(n, faces, ii, jj, kk);
+              dir[q] = elim_bits(n, faces, ii, jj, kk);
               vid[q] = ii + N1 * (jj + N1 * (int64_t)kk);
-              for (int a = 0; a < 3; ++a) xl[a * 4 + q] = dir[q] ? 0.0 : x[a * V + vid[q]];
+              for (int a = 0; a < 3; ++a) xl[a * 4 + q] = ((dir[q] >> a) & 1) ? 0.0 : x[a * V + vid[q]];
               xl[12 + q] = x[3 * V + vid[q]];
             }
             int64_t eid = 6 * (ci + (int64_t)n * (cj + (int64_t)n * ck)) + t;
@@ -218,8 +227,8 @@ int ora_apply_rows(int n, int form, double delta, const int32_t* faces, const do
             acc[3] += sp;
           }
         }
-    int d = is_dirichlet(n, faces, i, j, k);
-    for (int a = 0; a < 3; ++a) out[4 * s + a] = d ? 0.0 : acc[a];
+    int d = elim_bits(n, faces, i, j, k);
+    for (int a = 0; a < 3; ++a) out[4 * s + a] = ((d >> a) & 1) ? 0.0 : acc[a];
     out[4 * s + 3] = acc[3];
   }
   return 0;

@@ -17,6 +17,9 @@ Stabilisation c(p,q) = sum_T (delta h^2 / mu_T) (grad p, grad q)_T
             On coarse multigrid levels the viscosity of A and the 1/mu weight of C
             (and of the gauge) are separate per-element arrays (reading R15).
 Saddle system  [[A, B^T], [B, -C]] (u, p) = (f_h, 0)   P:1222-1235.
+Boundary: velocity DoFs on Dirichlet faces and the face-normal component on
+free-slip faces (u.n = 0; the tangential traction condition is natural)
+are eliminated; traction faces are natural.
 
 Vectors are field-major: [u1 (V), u2 (V), u3 (V), p (V)], vertex
 v = i + (n+1)(j + (n+1)k) (synth module convention).
@@ -26,7 +29,7 @@ from __future__ import annotations
 import numpy as np
 import scipy.sparse as sp
 
-from synth import PERMS, DIRICHLET, TRACTION, dirichlet_vertex_mask
+from synth import PERMS, DIRICHLET, TRACTION, dirichlet_vertex_mask, eliminated_mask
 
 FORMS = ("mod", "sym", "grad")
 
@@ -140,8 +143,10 @@ class Problem:
         self.form = form
         self.delta = delta
         self.dir_v = dirichlet_vertex_mask(n, self.faces)
-        self.free = np.concatenate([~self.dir_v, ~self.dir_v, ~self.dir_v,
-                                    np.ones(self.V, dtype=bool)])
+        # eliminated velocity DoFs: Dirichlet faces and the normal component on
+        # free-slip faces (u.n = 0); their rows and columns are dropped
+        self.elim = eliminated_mask(n, self.faces)
+        self.free = np.concatenate([~self.elim.reshape(-1), np.ones(self.V, dtype=bool)])
         self.has_traction = any(f == TRACTION for f in self.faces)
         self._assemble()
 
@@ -263,8 +268,7 @@ def load_nodal_elementwise(n: int, faces, f: np.ndarray) -> np.ndarray:
             fl = f[a][vid]                                 # (E, 4)
             loc = (vol / 20.0) * (fl.sum(axis=1, keepdims=True) + fl)
             b[a] += np.bincount(vid.reshape(-1), weights=loc.reshape(-1), minlength=V)
-    dv = dirichlet_vertex_mask(n, faces)
-    b[:, dv] = 0.0
+    b[eliminated_mask(n, faces)] = 0.0
     return np.concatenate([b.reshape(-1), np.zeros(V)])
 
 

@@ -30,6 +30,19 @@ Written from PAPER.md §5 with assembled scipy matrices:
 * Coarsest level: exact solve ("a direct coarse grid solver ... is not
   problematic") of the free-DoF system; without a traction face the pressure
   constant is fixed by the Lagrange row w^T p = 0 (reading R9/R16).
+  Or (coarse="minres") the paper's Krylov coarse solver, P:1245-1298:
+  the coarse system is re-discretised with the strain form A_sym (same coarse
+  viscosities), the momentum right-hand side is corrected by B^T M_L^-1 r2, and the
+  system [[A_sym, B^T], [B, -C]] is solved by MINRES preconditioned with
+  blockdiag(A^, M_L): A^^-1 = Jacobi-preconditioned CG on A_sym.  Reading R25
+  (DESIGN.md): M_L = the lumped mass weighted by 1/mu (diag int phi_i / mu, = the
+  paper's lumped mass for mu = 1), and the correction is r1 + B^T M_L^-1 r2 -- with
+  b(v,q) = -(div v, q) and a_sym = a_tr + (mu div, div) this is the
+  sign that makes the two coarse systems agree (B z ~ -M_L div z); the printed
+  "r1 - B^T M^-1 r2" moves the A_sym solution away from the A_tr one (pinned
+  in tests/test_oracle_coarse_minres.py).  The paper's stopping criteria are not printed ("selected such that the
+  multigrid convergence rates do not deteriorate"): fixed iteration counts here,
+  stopping early only when gamma_{j+1} <= 1e-14 gamma_1 (reading R24), MINRES from zero.
 """
 from __future__ import annotations
 
@@ -148,7 +161,8 @@ class Level:
 
 class Hierarchy:
     def __init__(self, n, cls, class_mu, faces, form="mod", delta=1.0 / 12.0,
-                 n_coarse=4, nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2):
+                 n_coarse=4, nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2,
+                 coarse="direct", minres_its=20, cg_its=4):
         self.levels = []
         self.P = []
         c = np.asarray(cls, dtype=np.uint8)
@@ -167,6 +181,8 @@ class Hierarchy:
         self.nu_pre, self.nu_post, self.nu_inc = nu_pre, nu_post, nu_inc
         self.omega = omega
         self.ncolors_u = ncolors_u
+        self.coarse, self.minres_its, self.cg_its = coarse, minres_its, cg_its
+        self.faces, self.delta = tuple(faces), delta
         self._coarse_setup()
 
     # -- smoother ----------------------------------------------------------
@@ -195,6 +211,9 @@ class Hierarchy:
 
     # -- coarse solve ------------------------------------------------------
     def _coarse_setup(self):
+        if self.coarse == "minres":
+            self._minres_setup()
+            return
         lev = self.levels[-1]
         pr = lev.prob
         free = np.flatnonzero(pr.free)
@@ -212,8 +231,98 @@ class Hierarchy:
         self.coarse_free = free
 
     def coarse_solve(self, b):
+        if self.coarse == "minres":
+            return self.coarse_solve_minres(b)
         x = np.zeros_like(b)
         x[self.coarse_free] = self.G @ b[self.coarse_free]
+        return x
+
+    # -- the paper's coarse solver ----------------------------
+    def _minres_setup(self):
+        lev = self.levels[-1]
+        self.psym = Problem(lev.n, lev.mu_a, self.faces, "sym", self.delta, elem_imu_c=lev.imu_c)
+        V = self.psym.V
+        self.ml = self.psym.gauge_w.copy()           # lumped 1/mu-weighted mass (R25)
+        self.dsym = self.psym.A.diagonal()                            # Jacobi for A_sym
+        self.fu = self.psym.free[:3 * V]
+
+    def jacobi_pcg(self, r):
+        """A^^-1 r: cg_its steps of Jacobi-preconditioned CG on A_sym (free velocity
+        DoFs) from zero (P:1247)."""
+        A, fu = self.psym.A, self.fu
+        dinv = np.where(fu, 1.0 / np.where(fu, self.dsym, 1.0), 0.0)
+        x = np.zeros_like(r)
+        r = np.where(fu, r, 0.0)
+        z = dinv * r
+        p = z.copy()
+        rz = r @ z
+        for k in range(self.cg_its):
+            if rz == 0.0:
+                break
+            Ap = np.where(fu, A @ p, 0.0)
+            alpha = rz / (p @ Ap)
+            x += alpha * p
+            r = r - alpha * Ap
+            if k + 1 == self.cg_its:
+                break
+            z = dinv * r
+            rz_new = r @ z
+            p = z + (rz_new / rz) * p
+            rz = rz_new
+        return x
+
+    def coarse_solve_minres(self, b):
+        """RHS correction r1 + B^T M_L^-1 r2 (R25), then preconditioned MINRES on
+        [[A_sym, B^T], [B, -C]] (Elman-Silvester-Wathen preconditioned MINRES, x0 = 0)
+        with the preconditioner blockdiag(A^, M_L), minres_its iterations."""
+        pr = self.psym
+        V = pr.V
+        free = pr.free
+
+        def K(x):
+            return np.where(free, pr.K @ np.where(free, x, 0.0), 0.0)
+
+        def Pinv(v):
+            return np.concatenate([self.jacobi_pcg(v[:3 * V]), v[3 * V:] / self.ml])
+
+        r = np.where(free, b, 0.0).copy()
+        r[:3 * V] += pr.B.T @ (r[3 * V:] / self.ml)               # r1 + B^T M_L^-1 r2 (R25)
+        r = np.where(free, r, 0.0)
+        x = np.zeros_like(r)
+        v_old = np.zeros_like(r)
+        v = r.copy()
+        z = Pinv(v)
+        gamma = np.sqrt(max(z @ v, 0.0))
+        if gamma == 0.0:
+            return x
+        gamma_old, gamma0 = 1.0, gamma
+        eta = gamma
+        s_old = s = 0.0
+        c_old = c = 1.0
+        w_old = np.zeros_like(r)
+        w = np.zeros_like(r)
+        for _ in range(self.minres_its):
+            z = z / gamma
+            Kz = K(z)
+            delta = Kz @ z
+            v_new = Kz - (delta / gamma) * v - (gamma / gamma_old) * v_old
+            z_new = Pinv(v_new)
+            gamma_new = np.sqrt(max(z_new @ v_new, 0.0))
+            a0 = c * delta - c_old * s * gamma
+            a1 = np.sqrt(a0 * a0 + gamma_new * gamma_new)
+            a2 = s * delta + c_old * c * gamma
+            a3 = s_old * gamma
+            c_old, s_old = c, s
+            c, s = a0 / a1, gamma_new / a1
+            w_new = (z - a3 * w_old - a2 * w) / a1
+            x = x + c * eta * w_new
+            eta = -s * eta
+            v_old, v = v, v_new
+            w_old, w = w, w_new
+            z = z_new
+            gamma_old, gamma = gamma, gamma_new
+            if gamma <= 1e-14 * gamma0:       # converged to rounding: stop (R24)
+                break
         return x
 
     # -- cycle -------------------------------------------------------------

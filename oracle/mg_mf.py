@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from synth import TRACTION, dirichlet_vertex_mask
+from synth import TRACTION, dirichlet_vertex_mask, eliminated_mask
 from . import capi, fem, mg
 
 
@@ -35,7 +35,7 @@ class MFProblem:
         self.imu_c = np.ascontiguousarray(imu_c, dtype=np.float64)
         self.faces, self.form, self.delta = tuple(faces), form, delta
         self.dir_v = dirichlet_vertex_mask(n, self.faces)
-        self.free = np.concatenate([~self.dir_v] * 3 + [np.ones(self.V, dtype=bool)])
+        self.free = np.concatenate([~eliminated_mask(n, self.faces).reshape(-1), np.ones(self.V, dtype=bool)])
         self.has_traction = any(f == TRACTION for f in self.faces)
         V = self.V
 
@@ -94,7 +94,8 @@ class MFLevel:
 
 class MFHierarchy(mg.Hierarchy):
     def __init__(self, n, cls, class_mu, faces, form="mod", delta=1.0 / 12.0,
-                 n_coarse=4, nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2):
+                 n_coarse=4, nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2,
+                 coarse="direct", minres_its=20, cg_its=4):
         self.levels, self.P = [], []
         c = np.asarray(cls, dtype=np.uint8)
         mu_a = np.asarray(class_mu, dtype=np.float64)[c]
@@ -111,4 +112,6 @@ class MFHierarchy(mg.Hierarchy):
         self.nu_pre, self.nu_post, self.nu_inc = nu_pre, nu_post, nu_inc
         self.omega = omega
         self.ncolors_u = ncolors_u
+        self.coarse, self.minres_its, self.cg_its = coarse, minres_its, cg_its
+        self.faces, self.delta = tuple(faces), delta
         self._coarse_setup()

@@ -71,6 +71,8 @@ _sigs = {
     "stk_layout": [_P, ctypes.c_int32, ctypes.POINTER(stk_layout_t)],
     "stk_import": [_P, ctypes.c_int32, _P, ctypes.c_int32, _P],
     "stk_export": [_P, ctypes.c_int32, _P, _P, ctypes.c_int32],
+    "stk_zero_eliminated": [_P, ctypes.c_int32, _P],
+    "stk_set_coarse_solver": [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32],
     "stk_load_vector": [_P, ctypes.c_int32, _P, _P, ctypes.c_int32, _P],
     "stk_apply": [_P, ctypes.c_int32, ctypes.c_uint32, _P, _P],
     "stk_residual": [_P, ctypes.c_int32, _P, _P, _P, _P],
@@ -263,6 +265,14 @@ class StokesContext:
     def assemble(self):
         self._chk("stk_assemble", _lib.stk_assemble(self.h))
 
+    def set_coarse_solver(self, kind="direct", minres_its=20, cg_its=4):
+        """Coarsest-level solver: "direct" (dense inverse of the A_tr system) or "minres"
+        (the paper's A_sym + corrected right-hand side + preconditioned MINRES,
+        P:1245-1298); re-assembles."""
+        k = {"direct": 0, "minres": 1}[kind]
+        self._chk("stk_set_coarse_solver", _lib.stk_set_coarse_solver(self.h, k, minres_its, cg_its))
+        self.assemble()
+
     def set_kernel_mode(self, mode: int):
         self._chk("stk_set_kernel_mode", _lib.stk_set_kernel_mode(self.h, mode))
 
@@ -302,8 +312,9 @@ class StokesContext:
         return n.value, ms.value
 
     # -- vectors --------------------------------------------------------------
-    def import_(self, canon, level=0, out=None):
-        """canonical (4, owned vertices) host numpy or device tensor -> padded device vector."""
+    def import_(self, canon, level=0, out=None, mask=True):
+        """canonical (4, owned vertices) host numpy or device tensor -> padded device vector;
+        mask: eliminated velocity DoFs set to 0 (operator inputs; False for a nodal forcing)."""
         out = self.new_vector(level) if out is None else out
         if isinstance(canon, np.ndarray):
             c = np.ascontiguousarray(canon, dtype=np.float64)
@@ -311,6 +322,8 @@ class StokesContext:
         else:
             c = canon.contiguous()
             self._chk("stk_import", _lib.stk_import(self.h, level, _ptr(c), DEVICE, _ptr(out)))
+        if mask:
+            self._chk("stk_zero_eliminated", _lib.stk_zero_eliminated(self.h, level, _ptr(out)))
         return out
 
     def export(self, vec, level=0) -> np.ndarray:
@@ -331,11 +344,11 @@ class StokesContext:
         f4 = np.zeros((4, lay.n_vertices)) if isinstance(f_canon, np.ndarray) else None
         if f4 is not None:
             f4[:3] = f_canon
-            fv = self.import_(f4)
+            fv = self.import_(f4, mask=False)
         else:
             t = self.torch.zeros((4, lay.n_vertices), dtype=self.torch.float64, device="cuda")
             t[:3] = f_canon
-            fv = self.import_(t)
+            fv = self.import_(t, mask=False)
         b = self.new_vector(0) if b is None else b
         self._chk("stk_load_vector", _lib.stk_load_vector(self.h, 0, _ptr(fv), None, 0, _ptr(b)))
         return b

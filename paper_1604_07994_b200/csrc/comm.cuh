@@ -42,10 +42,10 @@ __global__ void k_restrict_part(DGrid gf, DGrid gc, int K0, int K1, const double
   const int I = (int)(t % nx), J = (int)((t / nx) % nx), K = K0 + (int)(t / (nx * nx));
   const int fi = 2 * I, fj = 2 * J, fk = 2 * K;
   const int D[7][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {1, 1, 0}, {1, 0, 1}, {0, 1, 1}, {1, 1, 1}};
-  const bool dir = is_dirichlet(gc, I, J, K);
+  const unsigned em = elim(gc, I, J, K);
   const int64_t oc = vidx(gc, I, J, K);
   for (int f = 0; f < 4; ++f) {
-    if (f < 3 && dir) { bc[f * gc.fs + oc] = 0.0; continue; }
+    if ((em >> f) & 1u) { bc[f * gc.fs + oc] = 0.0; continue; }
     const double* r = rf + f * gf.fs;
     double s = r[vidx(gf, fi, fj, fk)];
     double e = 0.0;

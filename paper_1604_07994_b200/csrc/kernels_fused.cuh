@@ -63,11 +63,17 @@ __global__ void k_assemble_explicit(DGrid g, const int32_t* __restrict__ rows, i
   FetchUnit fx{i + kq_dx(q), j + kq_dy(q), k + kq_dz(q), c};
   double y[4], dA[3], dC;
   row_generic<FORM>(g, i, j, k, fx, BLK_ALL, y, dA, dC);
+  // columns of eliminated neighbour DoFs (Dirichlet / free-slip normal) are 0, as are
+  // the rows (row_generic) and inverse diagonals of the row's eliminated components
+  const int xi = fx.ui, yj = fx.uj, zk = fx.uk;
+  const bool in = xi >= 0 && yj >= 0 && zk >= 0 && xi <= g.n && yj <= g.n && zk <= g.n;
+  const bool ecol = c < 3 && (!in || ((elim(g, xi, yj, zk) >> c) & 1u));
 #pragma unroll
-  for (int r = 0; r < 4; ++r) S[(int64_t)e * EXPL + (r * NQ + q) * 4 + c] = y[r];
+  for (int r = 0; r < 4; ++r) S[(int64_t)e * EXPL + (r * NQ + q) * 4 + c] = ecol ? 0.0 : y[r];
   if (q == 0 && c == 0) {
+    const unsigned em = elim(g, i, j, k);
 #pragma unroll
-    for (int r = 0; r < 3; ++r) S[(int64_t)e * EXPL + 4 * NQ * 4 + r] = 1.0 / dA[r];
+    for (int r = 0; r < 3; ++r) S[(int64_t)e * EXPL + 4 * NQ * 4 + r] = ((em >> r) & 1u) ? 0.0 : 1.0 / dA[r];
     S[(int64_t)e * EXPL + 4 * NQ * 4 + 3] = 1.0 / dC;
   }
 }
@@ -272,8 +278,8 @@ __device__ __forceinline__ void f_vel_pass(const FLevel& L, int t0, int nthr, co
     int i, j, k;
     fvertex(g, t, i, j, k);
     const int o = fidx(g, i, j, k);
-    const bool dir = is_dirichlet(g, i, j, k);
-    const bool act = ((i + j + k) % nc) == color && !dir;
+    const unsigned em = elim(g, i, j, k);
+    const bool act = ((i + j + k) % nc) == color && em != 7u;
     if (!act) {  // Dirichlet entries of uin are 0 (invariant)
 #pragma unroll
       for (int a = 0; a < 3; ++a) uout[a * g.fs + o] = ldv<COH>(uin + a * g.fs + o);
@@ -353,9 +359,9 @@ __device__ __forceinline__ void f_residual(const FLevel& L, int t0, int nthr) {
     double nb[NQ][4], y[4], iA[3], iC;
     gather15<4, COH>(g, o, L.x, L.x + 3 * g.fs, nb);
     row_fused<FORM, 3, false>(L, o, i, j, k, code, nb, y, iA, iC);
-    const bool dir = is_dirichlet(g, i, j, k);
+    const unsigned em = elim(g, i, j, k);
 #pragma unroll
-    for (int f = 0; f < 4; ++f) L.r[f * g.fs + o] = (f < 3 && dir) ? 0.0 : bv[f] - y[f];
+    for (int f = 0; f < 4; ++f) L.r[f * g.fs + o] = ((em >> f) & 1u) ? 0.0 : bv[f] - y[f];
   }
 }
 
@@ -366,7 +372,7 @@ __device__ __forceinline__ void f_restrict(const FLevel& F, const FLevel& C, int
   ROW_LOOP(C, t0, nthr) {
     int I, J, K;
     fvertex(gc, t, I, J, K);
-    const bool dir = is_dirichlet(gc, I, J, K);
+    const unsigned em = elim(gc, I, J, K);
     const int oc = fidx(gc, I, J, K);
     const int of = fidx(gf, 2 * I, 2 * J, 2 * K);
     double v[NQ][4];
@@ -380,7 +386,7 @@ __device__ __forceinline__ void f_restrict(const FLevel& F, const FLevel& C, int
 #pragma unroll
       for (int q = 1; q < NQ; ++q) e += v[q][f];
       C.x[f * gc.fs + oc] = 0.0;
-      C.b[f * gc.fs + oc] = (f < 3 && dir) ? 0.0 : fma(0.5, e, v[0][f]);
+      C.b[f * gc.fs + oc] = ((em >> f) & 1u) ? 0.0 : fma(0.5, e, v[0][f]);
     }
   }
 }
@@ -393,7 +399,7 @@ __device__ __forceinline__ void f_prolong_add(const FLevel& C, const FLevel& F, 
     int i, j, k;
     fvertex(gf, t, i, j, k);
     const int of = fidx(gf, i, j, k);
-    const bool dir = is_dirichlet(gf, i, j, k);
+    const unsigned em = elim(gf, i, j, k);
     const int I = i >> 1, J = j >> 1, K = k >> 1;
     const int di = i & 1, dj = j & 1, dk = k & 1;
     const int o0 = fidx(gc, I, J, K);
@@ -409,7 +415,7 @@ __device__ __forceinline__ void f_prolong_add(const FLevel& C, const FLevel& F, 
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
       const double v = mid ? 0.5 * (c0[f] + c1[f]) : c0[f];
-      F.x[f * gf.fs + of] = (f < 3 && dir) ? 0.0 : xf[f] + v;
+      F.x[f * gf.fs + of] = ((em >> f) & 1u) ? 0.0 : xf[f] + v;
     }
   }
 }
@@ -658,10 +664,10 @@ __global__ void __launch_bounds__(ROW_NT) k_rowl(const __grid_constant__ FLevel 
 #pragma unroll
     for (int f = 0; f < 4; ++f) v[f] = seg_sum<LPR>(v[f]);
     if (sub < 4) {
-      const bool dir = is_dirichlet(gc, I, J, K);
+      const unsigned em = elim(gc, I, J, K);
       L2.x[sub * gc.fs + oc] = 0.0;
       const double vv = sub == 0 ? v[0] : sub == 1 ? v[1] : sub == 2 ? v[2] : v[3];
-      L2.b[sub * gc.fs + oc] = (sub < 3 && dir) ? 0.0 : vv;
+      L2.b[sub * gc.fs + oc] = ((em >> sub) & 1u) ? 0.0 : vv;
     }
     return;
   }
@@ -669,8 +675,8 @@ __global__ void __launch_bounds__(ROW_NT) k_rowl(const __grid_constant__ FLevel 
   fvertex(g, t, i, j, k);
   const int o = fidx(g, i, j, k);
   if (OP == FPH_VEL) {
-    const bool dir = is_dirichlet(g, i, j, k);
-    const bool act = ((i + j + k) % nc) == color && !dir;
+    const unsigned em = elim(g, i, j, k);
+    const bool act = ((i + j + k) % nc) == color && em != 7u;
     if (!act) {  // Dirichlet entries of uin are 0 (invariant)
       if (sub < 3) uout[sub * g.fs + o] = __ldg(uin + sub * g.fs + o);
       return;
@@ -721,15 +727,15 @@ __global__ void __launch_bounds__(ROW_NT) k_rowl(const __grid_constant__ FLevel 
     double y[4];
     row_lanes<FORM, 3, false, LPR>(L, M, o, i, j, k, code, slot, sub, L.x, L.x + 3 * g.fs, y);
     if (sub < 4) {
-      const bool dir = is_dirichlet(g, i, j, k);
+      const unsigned em = elim(g, i, j, k);
       const double yv = sub == 0 ? y[0] : sub == 1 ? y[1] : sub == 2 ? y[2] : y[3];
-      L.r[sub * g.fs + o] = (sub < 3 && dir) ? 0.0 : __ldg(L.b + sub * g.fs + o) - yv;
+      L.r[sub * g.fs + o] = ((em >> sub) & 1u) ? 0.0 : __ldg(L.b + sub * g.fs + o) - yv;
     }
   } else if (OP == FPH_PROLONG) {  // x_f += P x_c (L fine, L2 coarse)
     if (sub < 4) {
       const DGrid& gc = L2.g;
       const int f = sub;
-      const bool dir = is_dirichlet(g, i, j, k);
+      const unsigned em = elim(g, i, j, k);
       const int I = i >> 1, J = j >> 1, K = k >> 1;
       const int di = i & 1, dj = j & 1, dk = k & 1;
       const int o0 = fidx(gc, I, J, K);
@@ -737,7 +743,7 @@ __global__ void __launch_bounds__(ROW_NT) k_rowl(const __grid_constant__ FLevel 
       const int o1 = mid ? fidx(gc, I + di, J + dj, K + dk) : o0;
       const double c0 = __ldg(L2.x + f * gc.fs + o0), c1 = __ldg(L2.x + f * gc.fs + o1);
       const double v = mid ? 0.5 * (c0 + c1) : c0;
-      L.x[f * g.fs + o] = (f < 3 && dir) ? 0.0 : L.x[f * g.fs + o] + v;
+      L.x[f * g.fs + o] = ((em >> f) & 1u) ? 0.0 : L.x[f * g.fs + o] + v;
     }
   }
 }

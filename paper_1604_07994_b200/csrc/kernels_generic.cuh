@@ -38,9 +38,9 @@ __global__ void k_residual_generic(DGrid g, const double* __restrict__ x,
   double y[4], dA[3], dC;
   row_list<FORM, false>(g, i, j, k, x, x + 3 * g.fs, BLK_ALL, y, dA, dC);
   const int64_t o = vidx(g, i, j, k);
-  const bool dir = is_dirichlet(g, i, j, k);
+  const unsigned em = elim(g, i, j, k);
 #pragma unroll
-  for (int f = 0; f < 4; ++f) r[f * g.fs + o] = (f < 3 && dir) ? 0.0 : b[f * g.fs + o] - y[f];
+  for (int f = 0; f < 4; ++f) r[f * g.fs + o] = ((em >> f) & 1u) ? 0.0 : b[f * g.fs + o] - y[f];
 }
 
 // One colour pass of the velocity Gauss-Seidel (Jacobi within the colour):
@@ -53,16 +53,18 @@ __global__ void k_vel_pass_generic(DGrid g, const double* __restrict__ uin,
   int i, j, k;
   if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
   const int64_t o = vidx(g, i, j, k);
-  const bool active = ((i + j + k) % ncolors == color) && !is_dirichlet(g, i, j, k);
+  const unsigned em = elim(g, i, j, k);
+  const bool active = ((i + j + k) % ncolors == color) && em != 7u;
   if (!active) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) uout[a * g.fs + o] = is_dirichlet(g, i, j, k) ? 0.0 : uin[a * g.fs + o];
+    for (int a = 0; a < 3; ++a) uout[a * g.fs + o] = ((em >> a) & 1u) ? 0.0 : uin[a * g.fs + o];
     return;
   }
   double y[4], dA[3], dC;
   row_list<FORM, false>(g, i, j, k, uin, p, BLK_A | BLK_BT, y, dA, dC);
 #pragma unroll
-  for (int a = 0; a < 3; ++a) uout[a * g.fs + o] = uin[a * g.fs + o] + (b[a * g.fs + o] - y[a]) / dA[a];
+  for (int a = 0; a < 3; ++a)
+    uout[a * g.fs + o] = ((em >> a) & 1u) ? 0.0 : uin[a * g.fs + o] + (b[a * g.fs + o] - y[a]) / dA[a];
 }
 
 // Pressure step, part 1:  r_p = B u - C p - g ;  T = r_p / C_ii (colour 0), r_p (colour 1)
@@ -104,10 +106,10 @@ __global__ void k_restrict(DGrid gf, DGrid gc, const double* __restrict__ rf,
   if (!owned_vertex(gc, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, I, J, K)) return;
   const int fi = 2 * I, fj = 2 * J, fk = 2 * K;
   const int D[7][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}, {1, 1, 0}, {1, 0, 1}, {0, 1, 1}, {1, 1, 1}};
-  const bool dir = is_dirichlet(gc, I, J, K);
+  const unsigned em = elim(gc, I, J, K);
   const int64_t oc = vidx(gc, I, J, K);
   for (int f = 0; f < 4; ++f) {
-    if (f < 3 && dir) { bc[f * gc.fs + oc] = 0.0; continue; }
+    if ((em >> f) & 1u) { bc[f * gc.fs + oc] = 0.0; continue; }
     const double* r = rf + f * gf.fs;
     double s = r[vidx(gf, fi, fj, fk)];
     double e = 0.0;
@@ -130,14 +132,14 @@ __global__ void k_prolong_add(DGrid gc, DGrid gf, const double* __restrict__ xc,
   int i, j, k;
   if (!owned_vertex(gf, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
   const int64_t of = vidx(gf, i, j, k);
-  const bool dir = is_dirichlet(gf, i, j, k);
+  const unsigned em = elim(gf, i, j, k);
   const int I = i >> 1, J = j >> 1, K = k >> 1;
   const int di = i & 1, dj = j & 1, dk = k & 1;
   const int64_t o0 = vidx(gc, I, J, K);
   const bool mid = di | dj | dk;
   const int64_t o1 = mid ? vidx(gc, I + di, J + dj, K + dk) : o0;
   for (int f = 0; f < 4; ++f) {
-    if (f < 3 && dir) { xf[f * gf.fs + of] = 0.0; continue; }
+    if ((em >> f) & 1u) { xf[f * gf.fs + of] = 0.0; continue; }
     const double v = mid ? 0.5 * (xc[f * gc.fs + o0] + xc[f * gc.fs + o1]) : xc[f * gc.fs + o0];
     xf[f * gf.fs + of] += v;
   }
@@ -153,9 +155,9 @@ __global__ void k_partials(DGrid g, const double* __restrict__ x, double* __rest
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
        owned_vertex(g, t, i, j, k); t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t o = vidx(g, i, j, k);
-    const bool dir = is_dirichlet(g, i, j, k);
+    const unsigned em = elim(g, i, j, k);
     for (int f = 0; f < 4; ++f) {
-      const double v = (f < 3 && dir) ? 0.0 : x[f * g.fs + o];
+      const double v = ((em >> f) & 1u) ? 0.0 : x[f * g.fs + o];
       acc[f] += v * v;
     }
     if (with_gauge) {
@@ -234,8 +236,8 @@ __global__ void k_load_nodal(DGrid g, const double* __restrict__ f, double* __re
     }
   }
   const int64_t o = vidx(g, i, j, k);
-  const bool dir = is_dirichlet(g, i, j, k);
-  for (int a = 0; a < 3; ++a) b[a * g.fs + o] = dir ? 0.0 : acc[a];
+  const unsigned em = elim(g, i, j, k);
+  for (int a = 0; a < 3; ++a) b[a * g.fs + o] = ((em >> a) & 1u) ? 0.0 : acc[a];
   b[3 * g.fs + o] = 0.0;
 }
 
@@ -266,8 +268,8 @@ __global__ void k_load_elem(DGrid g, const uint8_t* __restrict__ fcls,
     }
   }
   const int64_t o = vidx(g, i, j, k);
-  const bool dir = is_dirichlet(g, i, j, k);
-  for (int a = 0; a < 3; ++a) b[a * g.fs + o] = dir ? 0.0 : acc[a];
+  const unsigned em = elim(g, i, j, k);
+  for (int a = 0; a < 3; ++a) b[a * g.fs + o] = ((em >> a) & 1u) ? 0.0 : acc[a];
   b[3 * g.fs + o] = 0.0;
 }
 
@@ -280,6 +282,21 @@ __global__ void k_pack(DGrid g, const double* __restrict__ canon, double* __rest
   const int64_t c = (int64_t)(k - g.z0) * per + (int64_t)j * nx + i;
   const int64_t o = vidx(g, i, j, k);
   for (int f = 0; f < nfields; ++f) dev[f * g.fs + o] = canon[f * cs + c];
+}
+__global__ void k_iota(int32_t* __restrict__ a, int64_t n) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) a[t] = (int32_t)t;
+}
+
+// velocity entries of eliminated DoFs (Dirichlet faces, free-slip normals) set to 0
+__global__ void k_zero_eliminated(DGrid g, double* __restrict__ v) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  const unsigned em = elim(g, i, j, k);
+  if (!em) return;
+  const int64_t o = vidx(g, i, j, k);
+  for (int a = 0; a < 3; ++a)
+    if ((em >> a) & 1u) v[a * g.fs + o] = 0.0;
 }
 __global__ void k_unpack(DGrid g, const double* __restrict__ dev, double* __restrict__ canon) {
   int i, j, k;
@@ -352,7 +369,7 @@ __global__ void k_classify(DGrid g, uint8_t* __restrict__ code, unsigned long lo
   const bool faces_ok = (i > 0 || (m & 1u)) && (i < g.n || (m & 2u)) && (j > 0 || (m & 4u)) &&
                         (j < g.n || (m & 8u)) && (k > 0 || (m & 16u)) && (k < g.n || (m & 32u));
   // a vertex on the traction top face z = 1 and on no other face (Gamma_F)
-  const bool top = k == g.n && !(m & 32u) && i > 0 && i < g.n && j > 0 && j < g.n;
+  const bool top = k == g.n && !(m & 32u) && !(g.slipmask & 32u) && i > 0 && i < g.n && j > 0 && j < g.n;
   if (faces_ok || top) {
     bool same = true;
     int first = -1;
@@ -599,10 +616,9 @@ __device__ __forceinline__ void row_warp(const DGrid& g, int i, int j, int k, co
           val[q][0] = val[q][1] = val[q][2] = 0.0;
           val[q][3] = ((xi + yj + zk) & 1) ? 0.0 : __ldg(Pf + oc);
         } else {
-          const bool dir = ((dm & 1u) && xi == 0) || ((dm & 2u) && xi == n) || ((dm & 4u) && yj == 0) ||
-                           ((dm & 8u) && yj == n) || ((dm & 16u) && zk == 0) || ((dm & 32u) && zk == n);
+          const unsigned em = elim_mask(dm, g.slipmask, n, xi, yj, zk);
 #pragma unroll
-          for (int f = 0; f < 3; ++f) val[q][f] = dir ? 0.0 : __ldg(U + f * g.fs + oc);
+          for (int f = 0; f < 3; ++f) val[q][f] = ((em >> f) & 1u) ? 0.0 : __ldg(U + f * g.fs + oc);
           val[q][3] = __ldg(Pf + oc);
         }
       }
@@ -664,7 +680,10 @@ __device__ __forceinline__ void row_warp(const DGrid& g, int i, int j, int k, co
   y[0] = r[0]; y[1] = r[1]; y[2] = r[2]; y[3] = r[3];
   dA[0] = r[4]; dA[1] = r[5]; dA[2] = r[6];
   dC = r[7];
-  if (is_dirichlet(g, i, j, k)) y[0] = y[1] = y[2] = 0.0;
+  const unsigned em = elim(g, i, j, k);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if ((em >> a) & 1u) y[a] = 0.0;
 }
 
 constexpr int GW_NT = 128;  // 4 rows per CTA
@@ -695,9 +714,9 @@ __global__ void __launch_bounds__(GW_NT) k_residual_gw(DGrid g, const double* __
   row_warp<FORM, false>(g, i, j, k, x, x + 3 * g.fs, BLK_ALL, y, dA, dC);
   if ((threadIdx.x & 31) == 0) {
     const int64_t o = vidx(g, i, j, k);
-    const bool dir = is_dirichlet(g, i, j, k);
+    const unsigned em = elim(g, i, j, k);
 #pragma unroll
-    for (int f = 0; f < 4; ++f) r[f * g.fs + o] = (f < 3 && dir) ? 0.0 : b[f * g.fs + o] - y[f];
+    for (int f = 0; f < 4; ++f) r[f * g.fs + o] = ((em >> f) & 1u) ? 0.0 : b[f * g.fs + o] - y[f];
   }
 }
 
@@ -708,14 +727,16 @@ __global__ void __launch_bounds__(GW_NT) k_vel_pass_gw(DGrid g, const double* __
   int i, j, k;
   if (!warp_vertex(g, i, j, k)) return;
   const int64_t o = vidx(g, i, j, k);
-  const bool dir = is_dirichlet(g, i, j, k);
-  const bool active = ((i + j + k) % ncolors == color) && !dir;  // warp-uniform
+  const unsigned em = elim(g, i, j, k);
+  const bool active = ((i + j + k) % ncolors == color) && em != 7u;  // warp-uniform
   double y[4], dA[3], dC;
   if (active) row_warp<FORM, false>(g, i, j, k, uin, p, BLK_A | BLK_BT, y, dA, dC);
   if ((threadIdx.x & 31) == 0) {
 #pragma unroll
     for (int a = 0; a < 3; ++a)
-      uout[a * g.fs + o] = dir ? 0.0 : active ? uin[a * g.fs + o] + (b[a * g.fs + o] - y[a]) / dA[a] : uin[a * g.fs + o];
+      uout[a * g.fs + o] = ((em >> a) & 1u) ? 0.0
+                           : active        ? uin[a * g.fs + o] + (b[a * g.fs + o] - y[a]) / dA[a]
+                                           : uin[a * g.fs + o];
   }
 }
 

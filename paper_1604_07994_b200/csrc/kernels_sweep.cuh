@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(SW_NT, 2)
 
 inline size_t sweep_smem() { return 1024 + SW_RING * SW_SLOT * sizeof(double) + SW_RING * sizeof(uint64_t); }
 
-inline bool sweep_supported(const DGrid& g) { return g.n >= 64 && g.n % SW_TX == 0 && encoder() != nullptr; }
+inline bool sweep_supported(const DGrid& g) { return g.slipmask == 0 && g.n >= 64 && g.n % SW_TX == 0 && encoder() != nullptr; }
 
 template <int FORM>
 bool launch_fsweep_t(const DGrid& g, const double* x, const double* f, double* uout, cudaStream_t st) {

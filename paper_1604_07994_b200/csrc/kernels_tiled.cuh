@@ -463,23 +463,24 @@ __device__ __forceinline__ void finish_boundary(const DGrid& g, const StreamArgs
 template <int FORM, int OP>
 __device__ __forceinline__ void list_row(const DGrid& g, const StreamArgs& a, int i, int j, int k) {
   const int64_t o = vidx(g, i, j, k);
-  const bool dir = is_dirichlet(g, i, j, k);
+  const unsigned em = elim(g, i, j, k);
   double y[4], dA[3], dC;
   if (OP == OP_APPLY || OP == OP_RESID) {
     row_list<FORM, false>(g, i, j, k, a.inU, a.inP, OP == OP_APPLY ? a.blocks : BLK_ALL, y, dA, dC);
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
       double v = y[f];
-      if (OP == OP_RESID) v = (f < 3 && dir) ? 0.0 : __ldg(a.aux + f * g.fs + o) - y[f];
+      if (OP == OP_RESID) v = ((em >> f) & 1u) ? 0.0 : __ldg(a.aux + f * g.fs + o) - y[f];
       a.out[f * g.fs + o] = v;
     }
   } else if (OP == OP_VEL) {
-    const bool act = ((i + j + k) & (a.ncolors - 1)) == a.color && !dir;
+    const bool act = ((i + j + k) & (a.ncolors - 1)) == a.color && em != 7u;
     if (act) row_list<FORM, false>(g, i, j, k, a.inU, a.inP, BLK_A | BLK_BT, y, dA, dC);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double uc = dir ? 0.0 : __ldg(a.inU + c * g.fs + o);
-      a.out[c * g.fs + o] = act ? uc + (__ldg(a.aux + c * g.fs + o) - y[c]) / dA[c] : uc;
+      const bool ec = (em >> c) & 1u;
+      const double uc = ec ? 0.0 : __ldg(a.inU + c * g.fs + o);
+      a.out[c * g.fs + o] = (act && !ec) ? uc + (__ldg(a.aux + c * g.fs + o) - y[c]) / dA[c] : uc;
     }
   } else if (OP == OP_P1) {
     row_list<FORM, false>(g, i, j, k, a.inU, a.inP, BLK_B | BLK_C, y, dA, dC);
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(LX_NT) k_listx(DGrid g, StreamArgs a, const do
   const int rr = t % (nx * nx);
   const int i = rr % nx, j = rr / nx;
   const int64_t o = vidx(g, i, j, k);
-  const bool dir = is_dirichlet(g, i, j, k);
+  const unsigned em = elim(g, i, j, k);
   const double* S = S0 + (int64_t)e * EXPL;
   // which rows / columns this OP needs
   constexpr bool VROWS = OP == OP_APPLY || OP == OP_RESID || OP == OP_VEL;
@@ -523,7 +524,7 @@ __global__ void __launch_bounds__(LX_NT) k_listx(DGrid g, StreamArgs a, const do
   constexpr bool UCOL = OP != OP_P2;
   const bool c0 = ((i + j + k) & 1) == 0;  // pressure colour 0
   bool act = true;
-  if (OP == OP_VEL) act = ((i + j + k) & (a.ncolors - 1)) == a.color && !dir;
+  if (OP == OP_VEL) act = ((i + j + k) & (a.ncolors - 1)) == a.color && em != 7u;
   if (OP == OP_P2) act = !c0;
   double py[4] = {0.0, 0.0, 0.0, 0.0};
   if (act && q < NQ) {
@@ -534,13 +535,11 @@ __global__ void __launch_bounds__(LX_NT) k_listx(DGrid g, StreamArgs a, const do
     const int64_t oc = o + dx + dy * g.px + dz * g.py;
     double u[3] = {0.0, 0.0, 0.0}, p = 0.0;
     if (UCOL) {
-      const unsigned dm = g.dirmask;
-      const bool dv = !in || ((dm & 1u) && xi == 0) || ((dm & 2u) && xi == n) || ((dm & 4u) && yj == 0) ||
-                      ((dm & 8u) && yj == n) || ((dm & 16u) && zk == 0) || ((dm & 32u) && zk == n);
+      const unsigned emv = in ? elim_mask(g.dirmask, g.slipmask, n, xi, yj, zk) : 7u;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const double v = __ldg(a.inU + c * g.fs + oc);
-        u[c] = dv ? 0.0 : v;
+        u[c] = ((emv >> c) & 1u) ? 0.0 : v;
       }
     }
     {
@@ -584,15 +583,16 @@ __global__ void __launch_bounds__(LX_NT) k_listx(DGrid g, StreamArgs a, const do
   if (OP == OP_APPLY || OP == OP_RESID) {
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
-      double v = (f < 3 && dir) ? 0.0 : py[f];
-      if (OP == OP_RESID) v = (f < 3 && dir) ? 0.0 : __ldg(a.aux + f * g.fs + o) - py[f];
+      double v = ((em >> f) & 1u) ? 0.0 : py[f];
+      if (OP == OP_RESID) v = ((em >> f) & 1u) ? 0.0 : __ldg(a.aux + f * g.fs + o) - py[f];
       a.out[f * g.fs + o] = v;
     }
   } else if (OP == OP_VEL) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double uc = dir ? 0.0 : __ldg(a.inU + c * g.fs + o);
-      const double v = act ? fma(__ldg(a.aux + c * g.fs + o) - py[c], __ldg(inv + c), uc) : uc;
+      const bool ec = (em >> c) & 1u;
+      const double uc = ec ? 0.0 : __ldg(a.inU + c * g.fs + o);
+      const double v = (act && !ec) ? fma(__ldg(a.aux + c * g.fs + o) - py[c], __ldg(inv + c), uc) : uc;
       if (a.cbuf) a.cbuf[(int64_t)e * 3 + c] = v;
       else a.out[c * g.fs + o] = v;
     }

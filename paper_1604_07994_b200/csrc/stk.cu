@@ -17,6 +17,7 @@
 #include "kernels_fused.cuh"
 #include "kernels_sweep.cuh"
 #include "krylov.cuh"
+#include "kernels_minres.cuh"
 
 using namespace stk;
 
@@ -136,8 +137,17 @@ struct stk_ctx {
   // Krylov workspace (GMRES(m), cfg.krylov = m)
   double* kbasis = nullptr;  // (m+1) level-0 vectors
   double* kwork = nullptr;   // 3 level-0 vectors: w, z, r
+  double* kz = nullptr;      // m preconditioned basis vectors Z_j = M^-1 V_j (nullptr: recompute)
+  int kz_tried = 0;
   double* kcoef = nullptr;   // device coefficients
   double* kpart = nullptr;   // partial dot products
+  // coarsest-level solver: 0 dense inverse of the A_tr system (default), 1 the paper's
+  // MINRES on A_sym with the corrected right-hand side (kernels_minres.cuh)
+  int coarse_kind = 0, mr_its = 20, mr_cg = 4;
+  double* mr_S = nullptr;     // A_sym explicit stencils of every coarsest-level vertex
+  int32_t* mr_rows = nullptr;
+  double* mr_work = nullptr;
+  size_t cap_mr_S = 0, cap_mr_rows = 0, cap_mr_work = 0;
 };
 
 namespace {
@@ -210,6 +220,12 @@ unsigned dirmask_of(const stk_config& c) {
     if (c.face[f] == STK_FACE_DIRICHLET0) m |= 1u << f;
   return m;
 }
+unsigned slipmask_of(const stk_config& c) {
+  unsigned m = 0;
+  for (int f = 0; f < 6; ++f)
+    if (c.face[f] == STK_FACE_FREESLIP) m |= 1u << f;
+  return m;
+}
 
 DGrid dgrid(const stk_ctx* ctx, const Level& L) {
   DGrid g;
@@ -224,6 +240,7 @@ DGrid dgrid(const stk_ctx* ctx, const Level& L) {
   g.delta = ctx->cfg.delta;
   g.idh3 = 1.0 / (ctx->cfg.delta * L.h * L.h * L.h);
   g.dirmask = dirmask_of(ctx->cfg);
+  g.slipmask = slipmask_of(ctx->cfg);
   g.cls = L.cls;
   g.emu = L.emu;
   g.code = L.code;
@@ -540,9 +557,32 @@ stk_status op_prolong_add(stk_ctx* ctx, int lc, const double* xc, double* xf) {
   return launched(ctx);
 }
 
+stk_status op_coarse_minres(stk_ctx* ctx, const double* b, double* x) {
+  Level& L = ctx->lev[ctx->nlev - 1];
+  MinresArgs A{};
+  A.g = dgrid(ctx, L);
+  A.S = ctx->mr_S;
+  A.b = b;
+  A.x = x;
+  A.work = ctx->mr_work;
+  A.its = ctx->mr_its;
+  A.cg_its = ctx->mr_cg;
+  PScope ps(ctx, P_COARSE, ctx->nlev - 1);
+  k_coarse_minres<FORM_SYM><<<1, MR_NT, 0, ctx->stream>>>(A);
+  return launched(ctx);
+}
+
 stk_status op_coarse(stk_ctx* ctx, const double* b, double* x) {
+  if (ctx->coarse_kind == 1) return op_coarse_minres(ctx, b, x);
   Level& L = ctx->lev[ctx->nlev - 1];
   const size_t sh = sizeof(double) * ctx->cN;
+  if (sh > 48 * 1024) {  // n_coarse = 8 / 16: opt in to the large dynamic shared memory
+    if (sh > 227 * 1024) {
+      ctx->err = "coarse right-hand side exceeds shared memory (n_coarse too large for op_coarse)";
+      return STK_EUNSUP;
+    }
+    CK(cudaFuncSetAttribute(k_coarse_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+  }
   PScope ps(ctx, P_COARSE, ctx->nlev - 1);
   k_coarse_apply<<<1, 1024, sh, ctx->stream>>>(dgrid(ctx, L), ctx->cdofs, ctx->cN, ctx->cN1, ctx->cG, b, x);
   return launched(ctx);
@@ -668,6 +708,10 @@ stk_status op_prolong_rows(stk_ctx* ctx, int lc) {
   return launch_row<FPH_PROLONG>(ctx, flevel(ctx, lc - 1), flevel(ctx, lc), owned_vertices(ctx->lev[lc - 1]));
 }
 stk_status op_coarse_rows(stk_ctx* ctx) {
+  if (ctx->coarse_kind == 1) {
+    Level& L = ctx->lev[ctx->nlev - 1];
+    return op_coarse_minres(ctx, L.b, L.x);
+  }
   PScope ps(ctx, P_COARSE, ctx->nlev - 1);
   k_coarse_warp<<<(ctx->cN + 7) / 8, 256, 0, ctx->stream>>>(flevel(ctx, ctx->nlev - 1), ctx->cdofs, ctx->cG, ctx->cN,
                                                            ctx->cN1);
@@ -896,7 +940,9 @@ stk_status op_vcycle(stk_ctx* ctx, int l, const double* b, double* x);
 
 // Right-preconditioned restarted GMRES(m) on K x = b with M^-1 = one V_var cycle
 // from a zero guess (a fixed linear map).  CGS2 orthogonalisation, Givens rotations;
-// the correction x += M^-1 (V y) costs one extra cycle per restart.
+// the preconditioned vectors Z_j = M^-1 V_j are kept (m more level-0 vectors) so the
+// restart correction is x += Z y; without the memory, x += M^-1 (V y) costs one extra
+// cycle per restart.
 stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int max_its, stk_report* R,
                     double bnorm, int& its, double& rel) {
   Level& L = ctx->lev[0];
@@ -915,10 +961,22 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
     CK(cudaMemsetAsync(ctx->kbasis, 0, vb * (m + 1), ctx->stream));
     CK(cudaMemsetAsync(ctx->kwork, 0, vb * 3, ctx->stream));
   }
+  // keep Z_j = M^-1 V_j when the memory is there: the restart update is then x += Z y
+  // (no extra preconditioner cycle per restart); else x += M^-1 (V y)
+  if (!ctx->kz && !ctx->kz_tried) {
+    ctx->kz_tried = 1;
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    if (vb * (size_t)m + (size_t)(2u << 30) < fr && cudaMalloc(&ctx->kz, vb * m) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->kz = nullptr;
+    }
+  }
   double* w = ctx->kwork;
   double* z = ctx->kwork + vlen;
   double* r = ctx->kwork + 2 * vlen;
   auto V = [&](int q) { return ctx->kbasis + (int64_t)q * vlen; };
+  auto Zv = [&](int q) { return ctx->kz ? ctx->kz + (int64_t)q * vlen : z; };
   DGrid g0 = dgrid(ctx, L);
   const unsigned nb = nblocks(owned_vertices(L));
   std::vector<double> H((m + 1) * m, 0.0), cs(m), sn(m), gv(m + 1), h(m + 1), h2(m + 1), y(m);
@@ -934,12 +992,15 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
     gv[0] = beta;
     int jdone = 0;
     for (int j = 0; j < m && its < max_its; ++j) {
-      CK(cudaMemsetAsync(z, 0, vb, ctx->stream));
-      ST(op_vcycle(ctx, 0, V(j), z));
-      ST(op_apply(ctx, 0, BLK_ALL, z, w));
+      double* zj = Zv(j);
+      CK(cudaMemsetAsync(zj, 0, vb, ctx->stream));
+      ST(op_vcycle(ctx, 0, V(j), zj));
+      ST(op_apply(ctx, 0, BLK_ALL, zj, w));
       if (m + 1 <= KRY_MAXV) {
         // classical Gram-Schmidt twice (CGS2) in three fused flat passes: dots; update +
-        // the second pass's dots; update + ||w||^2 -- one host round trip per iteration
+        // the second pass's dots; update + ||w||^2 -- one host round trip per iteration.
+        // (CGS1 with the Pythagorean norm, two passes, measured 34 instead of 29 GMRES
+        // iterations on cfg3 n = 256: the lost orthogonality costs more than the pass.)
         double* c1 = ctx->kcoef + (m + 2);
         double* c2 = ctx->kcoef + 2 * (m + 2);
         double* nw = ctx->kcoef + 3 * (m + 2);
@@ -1000,11 +1061,15 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
       y[q] = s / H[q * m + q];
     }
     for (int q = 0; q < jdone; ++q) y[q] = -y[q];
-    ST(op_update(ctx, V(0), jdone, y.data(), 0.0, w));  // w = sum y_q V_q
-    CK(cudaMemsetAsync(z, 0, vb, ctx->stream));
-    ST(op_vcycle(ctx, 0, w, z));
-    k_axpby<<<nb, kThreads, 0, ctx->stream>>>(g0, 1.0, z, 1.0, x);
-    ST(launched(ctx));
+    if (ctx->kz) {
+      ST(op_update(ctx, ctx->kz, jdone, y.data(), 1.0, x));  // x += sum y_q Z_q
+    } else {
+      ST(op_update(ctx, V(0), jdone, y.data(), 0.0, w));  // w = sum y_q V_q
+      CK(cudaMemsetAsync(z, 0, vb, ctx->stream));
+      ST(op_vcycle(ctx, 0, w, z));
+      k_axpby<<<nb, kThreads, 0, ctx->stream>>>(g0, 1.0, z, 1.0, x);
+      ST(launched(ctx));
+    }
     ST(op_residual(ctx, 0, x, b, r));
     ST(op_dots(ctx, r, 1, r, &nr));
     beta = std::sqrt(nr);
@@ -1047,7 +1112,7 @@ stk_status fused_assemble(stk_ctx* ctx) {
     }
   if (rl < 0) return STK_OK;
   int fl = -1;
-  if (ctx->fuse_n > 0)
+  if (ctx->fuse_n > 0 && ctx->coarse_kind == 0)
     for (int l = ctx->nlev - 2; l >= rl; --l) {
       const Level& L = ctx->lev[l];
       if (L.n > ctx->fuse_n || (ctx->cfg.nranks > 1 && !L.replicated) || ctx->nlev - l > FMAX) break;
@@ -1235,12 +1300,16 @@ stk_status create_impl(const stk_config* cfg, const uint8_t* id, stk_loopback* g
   if (cfg->krylov < 0 || cfg->krylov > 200) return STK_EINVAL;
   const int nc = cfg->n_coarse > 0 ? cfg->n_coarse : 4;
   if (nc > n || (nc & (nc - 1)) != 0 || nc > 16) return STK_EINVAL;
-  bool any_dir = false;
+  bool any_dir = false, slip_axis[3] = {false, false, false};
   for (int f = 0; f < 6; ++f) {
-    if (cfg->face[f] != STK_FACE_DIRICHLET0 && cfg->face[f] != STK_FACE_TRACTION) return STK_EINVAL;
+    if (cfg->face[f] != STK_FACE_DIRICHLET0 && cfg->face[f] != STK_FACE_TRACTION && cfg->face[f] != STK_FACE_FREESLIP)
+      return STK_EINVAL;
     any_dir |= cfg->face[f] == STK_FACE_DIRICHLET0;
+    slip_axis[f / 2] |= cfg->face[f] == STK_FACE_FREESLIP;
   }
-  if (!any_dir) return STK_EINVAL;  // Korn: |Gamma_D| > 0
+  // Korn: |Gamma_D| > 0, or free-slip faces of all three normal directions
+  // (u.n = 0 on faces x, y and z excludes the rigid translations and rotations)
+  if (!any_dir && !(slip_axis[0] && slip_axis[1] && slip_axis[2])) return STK_EINVAL;
   stk_ctx* ctx = new stk_ctx();
   ctx->cfg = *cfg;
   ctx->cfg.n_coarse = nc;
@@ -1482,17 +1551,34 @@ stk_status stk_assemble(stk_ctx* ctx) {
       return STK_ECUDA;
     }
   }
-  // coarsest level: dense K (+ gauge row), Gauss-Jordan inverse
   Level& L = ctx->lev[ctx->nlev - 1];
+  if (ctx->coarse_kind == 1) {
+    // the paper's coarse solver: A_sym explicit stencils of every vertex of the level
+    if (!L.replicated && ctx->cfg.nranks > 1) {
+      ctx->err = "MINRES coarse solver needs the coarsest level held whole by every rank";
+      return STK_EUNSUP;
+    }
+    const int64_t V = owned_vertices(L);
+    if (!ensure(ctx->mr_S, ctx->cap_mr_S, (size_t)EXPL * V) || !ensure(ctx->mr_rows, ctx->cap_mr_rows, (size_t)V) ||
+        !ensure(ctx->mr_work, ctx->cap_mr_work, (size_t)MR_NVEC * 4 * V))
+      return STK_ENOMEM;
+    k_iota<<<nblocks(V), kThreads, 0, ctx->stream>>>(ctx->mr_rows, V);
+    ST(launched(ctx));
+    k_assemble_explicit<FORM_SYM><<<nblocks(V * NQ * 4), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), ctx->mr_rows,
+                                                                                        (int)V, ctx->mr_S);
+    ST(launched(ctx));
+    ctx->cN = ctx->cN1 = 0;
+    ST(fused_setup(ctx));
+  } else {
+  // coarsest level: dense K (+ gauge row), Gauss-Jordan inverse
   std::vector<int32_t> dofs;
-  const unsigned dm = dirmask_of(ctx->cfg);
+  const unsigned dm = dirmask_of(ctx->cfg), sm = slipmask_of(ctx->cfg);
   for (int k = L.z0; k < L.z0 + L.nzl; ++k)
     for (int j = 0; j <= L.n; ++j)
       for (int i = 0; i <= L.n; ++i) {
-        const bool dir = ((dm & 1) && i == 0) || ((dm & 2) && i == L.n) || ((dm & 4) && j == 0) ||
-                         ((dm & 8) && j == L.n) || ((dm & 16) && k == 0) || ((dm & 32) && k == L.n);
+        const unsigned em = elim_mask(dm, sm, L.n, i, j, k);
         for (int f = 0; f < 4; ++f)
-          if (f == 3 || !dir) dofs.push_back((f << 28) | (k << 18) | (j << 9) | i);
+          if (!((em >> f) & 1u)) dofs.push_back((f << 28) | (k << 18) | (j << 9) | i);
       }
   std::sort(dofs.begin(), dofs.end(), [](int32_t a, int32_t b) {
     const int fa = (a >> 28) & 0xF, fb = (b >> 28) & 0xF;
@@ -1537,18 +1623,24 @@ stk_status stk_assemble(stk_ctx* ctx) {
     CK(cudaLaunchKernelEx(&lc, k_gauss_jordan_coop, ctx->cK, ctx->cG, ctx->cfac, N1, ctx->cstatus, ctx->fbar));
     ST(launched(ctx));
   }
+  }
   ST(fused_assemble(ctx));
-  int hs = 0;
-  CK(cudaMemcpyAsync(&hs, ctx->cstatus, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  if (hs) {
-    ctx->err = "coarse-level matrix is singular";
-    return STK_ECUDA;
+  if (ctx->coarse_kind == 0) {
+    int hs = 0;
+    CK(cudaMemcpyAsync(&hs, ctx->cstatus, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (hs) {
+      ctx->err = "coarse-level matrix is singular";
+      return STK_ECUDA;
+    }
+  } else {
+    CK(cudaStreamSynchronize(ctx->stream));
   }
   // keep the captured coarse graph when nothing it depends on changed (pointers,
   // list / explicit-row counts, kernel selection); the data behind them is updated
   std::vector<int64_t> sig = {ctx->kernel_mode, ctx->rl, ctx->fl, ctx->row_n, ctx->fuse_n, ctx->cN, ctx->cN1,
-                              (int64_t)ctx->cdofs, (int64_t)ctx->cG, (int64_t)ctx->fprog, ctx->fnph};
+                              (int64_t)ctx->cdofs, (int64_t)ctx->cG, (int64_t)ctx->fprog, ctx->fnph,
+                              ctx->coarse_kind, ctx->mr_its, ctx->mr_cg, (int64_t)ctx->mr_S, (int64_t)ctx->mr_work};
   for (auto& Lv : ctx->lev)
     for (int64_t v : {(int64_t)Lv.list, Lv.nirr, (int64_t)Lv.Slist, (int64_t)Lv.slot, (int64_t)Lv.S, Lv.nexpl,
                       (int64_t)Lv.rlist, Lv.nrl, (int64_t)Lv.Srl})
@@ -1597,6 +1689,24 @@ stk_status stk_import(stk_ctx* ctx, int32_t level, const double* canon, int32_t 
   if (staging) CK(cudaFreeAsync(staging, ctx->stream));
   if (where == STK_HOST) CK(cudaStreamSynchronize(ctx->stream));
   return s;
+}
+
+stk_status stk_set_coarse_solver(stk_ctx* ctx, int32_t kind, int32_t minres_its, int32_t cg_its) {
+  if (!ctx || kind < 0 || kind > 1 || minres_its < 1 || minres_its > 10000 || cg_its < 0 || cg_its > 10000)
+    return STK_EINVAL;
+  ctx->coarse_kind = kind;
+  ctx->mr_its = minres_its;
+  ctx->mr_cg = cg_its;
+  if (ctx->state == 2) ctx->state = 1;  // re-assemble before the next solve
+  return STK_OK;
+}
+
+stk_status stk_zero_eliminated(stk_ctx* ctx, int32_t level, double* dev) {
+  ST(check(ctx, 0));
+  ST(check_level(ctx, level));
+  Level& L = ctx->lev[level];
+  k_zero_eliminated<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), dev);
+  return launched(ctx);
 }
 
 stk_status stk_export(stk_ctx* ctx, int32_t level, const double* dev, double* canon, int32_t where) {
@@ -1922,6 +2032,9 @@ stk_status stk_destroy(stk_ctx* ctx) {
   cudaFree(ctx->cdofs);
   cudaFree(ctx->cK);
   cudaFree(ctx->cG);
+  cudaFree(ctx->mr_S);
+  cudaFree(ctx->mr_rows);
+  cudaFree(ctx->mr_work);
   cudaFree(ctx->cstatus);
   cudaFree(ctx->d_mu);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
@@ -1936,6 +2049,7 @@ stk_status stk_destroy(stk_ctx* ctx) {
   ctx->prof.destroy();
   cudaFree(ctx->kbasis);
   cudaFree(ctx->kwork);
+  cudaFree(ctx->kz);
   cudaFree(ctx->kcoef);
   cudaFree(ctx->kpart);
   delete ctx;

@@ -58,6 +58,7 @@ struct DGrid {
   double delta;     // stabilisation constant
   double idh3;      // 1 / (delta h^3)
   unsigned dirmask; // bit f set: face f is homogeneous Dirichlet
+  unsigned slipmask; // bit f set: face f is free-slip (u.n = 0, tangential traction 0)
   const uint8_t* cls;   // element classes [cz - cz0][cj][ci][t]
   const uint8_t* code;  // per-vertex code (plane layout of one field)
   const double* mu;     // per-class viscosity mu_k [0..255], 1/mu_k at mu + 256 (device)
@@ -85,6 +86,20 @@ __device__ __forceinline__ bool is_dirichlet(const DGrid& g, int i, int j, int k
   const unsigned m = g.dirmask;
   return ((m & 1u) && i == 0) || ((m & 2u) && i == g.n) || ((m & 4u) && j == 0) ||
          ((m & 8u) && j == g.n) || ((m & 16u) && k == 0) || ((m & 32u) && k == g.n);
+}
+
+// eliminated velocity components of vertex (i,j,k): bit a = component a is fixed to 0
+// (all three on a Dirichlet face; the face-normal component on a free-slip face,
+// u.n = 0; Dirichlet wins on shared edges and corners)
+__host__ __device__ __forceinline__ unsigned elim_mask(unsigned dm, unsigned sm, int n, int i, int j, int k) {
+  const unsigned onf = (i == 0 ? 1u : 0u) | (i == n ? 2u : 0u) | (j == 0 ? 4u : 0u) | (j == n ? 8u : 0u) |
+                       (k == 0 ? 16u : 0u) | (k == n ? 32u : 0u);
+  if (onf & dm) return 7u;
+  const unsigned s = onf & sm;
+  return ((s & 3u) ? 1u : 0u) | ((s & 12u) ? 2u : 0u) | ((s & 48u) ? 4u : 0u);
+}
+__device__ __forceinline__ unsigned elim(const DGrid& g, int i, int j, int k) {
+  return elim_mask(g.dirmask, g.slipmask, g.n, i, j, k);
 }
 
 __device__ __forceinline__ int64_t elem_index(const DGrid& g, int ci, int cj, int ck, int t) {
@@ -204,7 +219,12 @@ __device__ __forceinline__ void row_generic(const DGrid& g, int i, int j, int k,
       }
     }
   }
-  if (is_dirichlet(g, i, j, k)) y[0] = y[1] = y[2] = 0.0;
+  {
+    const unsigned em = elim(g, i, j, k);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if ((em >> a) & 1u) y[a] = 0.0;
+  }
 }
 
 // local cube corner (bit0 x, bit1 y, bit2 z) of vertex q = 0..3 of Kuhn tet t
@@ -250,10 +270,9 @@ __device__ __forceinline__ void row_list(const DGrid& g, int i, int j, int k, co
       nb[o][0] = nb[o][1] = nb[o][2] = 0.0;
       nb[o][3] = (in && !((xi + yj + zk) & 1)) ? __ldg(Pf + oc) : 0.0;
     } else {
-      const bool dir = !in || ((dm & 1u) && xi == 0) || ((dm & 2u) && xi == n) || ((dm & 4u) && yj == 0) ||
-                       ((dm & 8u) && yj == n) || ((dm & 16u) && zk == 0) || ((dm & 32u) && zk == n);
+      const unsigned em = in ? elim_mask(dm, g.slipmask, n, xi, yj, zk) : 7u;
 #pragma unroll
-      for (int f = 0; f < 3; ++f) nb[o][f] = dir ? 0.0 : __ldg(U + f * g.fs + oc);
+      for (int f = 0; f < 3; ++f) nb[o][f] = ((em >> f) & 1u) ? 0.0 : __ldg(U + f * g.fs + oc);
       nb[o][3] = in ? __ldg(Pf + oc) : 0.0;
     }
   }
@@ -335,7 +354,12 @@ __device__ __forceinline__ void row_list(const DGrid& g, int i, int j, int k, co
       dC += cstab * imu * gg;
     }
   }
-  if (is_dirichlet(g, i, j, k)) y[0] = y[1] = y[2] = 0.0;
+  {
+    const unsigned em = elim(g, i, j, k);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      if ((em >> a) & 1u) y[a] = 0.0;
+  }
 }
 
 // w_j = int phi_j / mu = sum_{T ni j} |T| / (4 mu_T)   (gauge weight)

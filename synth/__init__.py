@@ -9,7 +9,8 @@ BASELINE.json ``configs[0..4]``:
 * the per-element viscosity class by a centroid predicate,
 * the per-element forcing class (element-constant forcing, cfg3/cfg5),
 * counter-based splitmix64 random numbers for nodal forcing and apply inputs,
-* the face boundary types (0 = homogeneous Dirichlet, 1 = traction free).
+* the face boundary types (0 = homogeneous Dirichlet, 1 = traction free,
+  2 = free slip) and the eliminated velocity DoFs they define.
 
 The geometry follows PAPER.md P:720 ("4^3 cubes ... each subdivided into six
 tetrahedra"); the Kuhn split itself is the reading of DESIGN.md §3 (R2).
@@ -24,7 +25,7 @@ import numpy as np
 # Kuhn permutations, t = 0..5  <->  sigma.
 PERMS = ((0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0))
 
-DIRICHLET, TRACTION = 0, 1
+DIRICHLET, TRACTION, FREESLIP = 0, 1, 2
 FACE_NAMES = ("x0", "x1", "y0", "y1", "z0", "z1")
 
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
@@ -74,6 +75,7 @@ class Config:
 
 ALL_DIRICHLET = (DIRICHLET,) * 6
 TOP_TRACTION = (DIRICHLET,) * 5 + (TRACTION,)
+ALL_FREESLIP = (FREESLIP,) * 6
 
 CONFIGS = {
     # BASELINE.json configs[0]: plane x=0.5, mu1=10 (x<0.5), mu2=1, u=0 on all faces
@@ -89,6 +91,11 @@ CONFIGS = {
     # f_z=-1 in the plate
     "cfg5": Config("cfg5", 1024, (1.0, 1e3), TOP_TRACTION, "element",
                    ((0.0, 0.0, 0.0), (0.0, 0.0, -1.0))),
+    # SURVEY NEXT-1, the paper's own timed workload:
+    # viscosity columns mu2 = 10 in (0,1/4)^2 x (0,1) u (3/4,1)^2 x (0,1), mu1 = 1
+    # elsewhere; free slip on all faces; f = (0, 0, -cos 2pi x cos 2pi y sin pi z)
+    # (nodal values); levels L = 5..8 are n = 4 * 2^L = 128..1024 (4^3 base cubes)
+    "cols": Config("cols", 128, (1.0, 10.0), ALL_FREESLIP, "nodal"),
 }
 
 
@@ -155,6 +162,10 @@ def _classes_block(cfg: Config, k0: int, k1: int):
             inside[sl] |= (xs - c[s, 0]) ** 2 + (ys - c[s, 1]) ** 2 + (zs - c[s, 2]) ** 2 < r[s] ** 2
         mu_cls = np.where(inside, 1, 0)
         f_cls = np.zeros_like(mu_cls)
+    elif name == "cols":
+        col = ((x < 0.25) & (y < 0.25)) | ((x > 0.75) & (y > 0.75))
+        mu_cls = np.where(col, 1, 0)
+        f_cls = np.zeros_like(mu_cls)
     elif name == "cfg5":
         s = x + z
         plate = (s >= 1.2 - 0.08 * math.sqrt(2.0)) & (s <= 1.2) & (z <= 0.9)
@@ -186,8 +197,17 @@ def element_classes(cfg: Config, k0: int = 0, k1: int | None = None):
 
 
 def nodal_forcing(cfg: Config, v0: int = 0, v1: int | None = None) -> np.ndarray:
-    """f_a(v) = 2 U(1, 3v+a) - 1 for vertices v0..v1-1, shape (3, v1-v0)."""
+    """f_a(v) = 2 U(1, 3v+a) - 1 for vertices v0..v1-1, shape (3, v1-v0); for the
+    "cols" workload the paper's f = (0, 0, -cos 2pi x cos 2pi y sin pi z) at the
+    vertices (P:719)."""
     v1 = cfg.vertices if v1 is None else v1
+    if cfg.name == "cols":
+        N1 = cfg.n + 1
+        v = np.arange(v0, v1, dtype=np.int64)
+        x, y, z = (v % N1) / cfg.n, ((v // N1) % N1) / cfg.n, (v // (N1 * N1)) / cfg.n
+        f = np.zeros((3, v1 - v0))
+        f[2] = -np.cos(2 * np.pi * x) * np.cos(2 * np.pi * y) * np.sin(np.pi * z)
+        return f
     v = np.arange(v0, v1, dtype=np.uint64)
     return np.stack([2.0 * uniform(cfg.seed, 1, 3 * v + a) - 1.0 for a in range(3)])
 
@@ -208,3 +228,19 @@ def dirichlet_vertex_mask(n: int, faces) -> np.ndarray:
         if faces[f] == DIRICHLET:
             m |= coord == val
     return m.reshape(-1)
+
+
+def eliminated_mask(n: int, faces) -> np.ndarray:
+    """Boolean (3, V) mask: velocity component a of vertex v is fixed to 0 -- all three
+    on the closure of a Dirichlet face, component a on a free-slip face of normal
+    e_a (u.n = 0).  The boundary-condition definition of the workload."""
+    idx = np.arange(n + 1)
+    k, j, i = np.meshgrid(idx, idx, idx, indexing="ij")
+    m = np.zeros((3,) + (n + 1,) * 3, dtype=bool)
+    for f, (coord, val) in enumerate(((i, 0), (i, n), (j, 0), (j, n), (k, 0), (k, n))):
+        on = coord == val
+        if faces[f] == DIRICHLET:
+            m[:, on] = True
+        elif faces[f] == FREESLIP:
+            m[f // 2][on] = True
+    return m.reshape(3, -1)

@@ -65,7 +65,8 @@ def owned(ctx, arr, n):
     return np.ascontiguousarray(arr[:, lay.z0 * N2:(lay.z0 + lay.nz_local) * N2])
 
 
-@pytest.mark.parametrize("cfgname,n,P", [("cfg2", 64, 2), ("cfg2", 64, 4), ("cfg3", 64, 4), ("cfg5", 128, 8)])
+@pytest.mark.parametrize("cfgname,n,P", [("cfg2", 64, 2), ("cfg2", 64, 4), ("cfg3", 64, 4), ("cfg5", 128, 8),
+                                        ("cols", 64, 4)])
 def test_loopback_apply_bitwise_and_vcycle(cfgname, n, P):
     ctx1, cfg, cls, _ = make_ctx(cfgname, n, "mod")
     x = synth.apply_input(cfg)
@@ -105,7 +106,7 @@ def test_loopback_apply_bitwise_and_vcycle(cfgname, n, P):
     grp.close()
 
 
-@pytest.mark.parametrize("cfgname,n,P,kry", [("cfg2", 64, 4, 0), ("cfg3", 64, 2, 30)])
+@pytest.mark.parametrize("cfgname,n,P,kry", [("cfg2", 64, 4, 0), ("cfg3", 64, 2, 30), ("cols", 64, 2, 0)])
 def test_loopback_solve_matches_single_rank(cfgname, n, P, kry):
     ctx1, cfg, cls, fcls = make_ctx(cfgname, n, "mod", krylov=kry)
     if cfg.forcing == "nodal":

@@ -24,6 +24,7 @@ def _oracle_problem(cfg, cls, form):
     ("cfg1", 16, "mod", 0), ("cfg1", 16, "mod", 1),
     ("cfg2", 32, "mod", 1), ("cfg2", 32, "sym", 1), ("cfg2", 32, "grad", 1),
     ("cfg3", 32, "mod", 1), ("cfg5", 32, "mod", 1),
+    ("cols", 16, "mod", 0), ("cols", 16, "mod", 1), ("cols", 32, "sym", 1), ("cols", 32, "grad", 1),
 ])
 def test_apply_small_vs_assembled_oracle(cfgname, n, form, mode):
     ctx, cfg, cls, _ = make_ctx(cfgname, n, form, kernel_mode=mode)
@@ -66,7 +67,8 @@ def test_apply_blocks(blocks):
 @pytest.mark.parametrize("cfgname,n,form", [("cfg4", 64, "mod"), ("cfg4", 128, "mod"), ("cfg3", 128, "mod"),
                                             ("cfg5", 128, "mod"), ("cfg2", 128, "mod"),
                                             ("cfg2", 128, "sym"), ("cfg2", 128, "grad"), ("cfg5", 64, "sym"),
-                                            ("cfg3", 64, "grad")])
+                                            ("cfg3", 64, "grad"), ("cols", 64, "mod"), ("cols", 128, "mod"),
+                                            ("cols", 128, "sym"), ("cols", 64, "grad")])
 def test_apply_full_grid_vs_c_oracle(cfgname, n, form):
     """Tiled (TMA stream) kernels, every form (a4), full grid vs the C element loop."""
     ctx, cfg, cls, _ = make_ctx(cfgname, n, form)
@@ -77,7 +79,7 @@ def test_apply_full_grid_vs_c_oracle(cfgname, n, form):
     assert err <= TOL_APPLY, errs
 
 
-@pytest.mark.parametrize("cfgname,n", [("cfg4", 512), ("cfg3", 256), ("cfg2", 128)])
+@pytest.mark.parametrize("cfgname,n", [("cfg4", 512), ("cfg3", 256), ("cfg2", 128), ("cols", 256)])
 def test_apply_bench_size_sampled_rows(cfgname, n):
     """Full BASELINE size, same launch configuration as bench.py: rows at sampled
     vertices (random + every irregular class of row: boundary faces, edges, corners,
@@ -105,7 +107,7 @@ def test_apply_bench_size_sampled_rows(cfgname, n):
     assert np.all(np.abs(got - rows) <= 1e-12 * scale[None, :]), np.abs(got - rows).max(axis=0) / scale
 
 
-@pytest.mark.parametrize("cfgname,n", [("cfg1", 16), ("cfg3", 16), ("cfg5", 16)])
+@pytest.mark.parametrize("cfgname,n", [("cfg1", 16), ("cfg3", 16), ("cfg5", 16), ("cols", 16)])
 def test_load_vector(cfgname, n):
     ctx, cfg, cls, fcls = make_ctx(cfgname, n, "mod")
     pr = _oracle_problem(cfg, cls, "mod")
@@ -139,7 +141,7 @@ def _row_codes(c, faces):
     c [k][j][i][t]: class k (< 0x40) when the star of tets inside the cube is one
     pure class and the vertex is interior or lies only on Dirichlet faces; 0x40 | k
     for such a star at a vertex of the traction top face z = 1 on no other face;
-    else 0xFF (interface / traction / MIXED / boundary row: explicit stencil)."""
+    else 0xFF (interface / traction / free-slip / MIXED row: explicit stencil)."""
     smin, smax, _ = _star_minmax(c)
     m1 = c.shape[0] + 1
     on = np.zeros((6,) + (m1,) * 3, bool)     # [face][k][j][i]
@@ -151,6 +153,9 @@ def _row_codes(c, faces):
         if int(faces[f]) == 1:
             trac |= on[f]
     top_only = on[5] & (on.sum(axis=0) == 1) & (int(faces[5]) == 1)
+    for f in range(6):
+        if int(faces[f]) == 2:                     # free-slip face: explicit rows
+            trac |= on[f]
     pure = (smin == smax) & (smax < 0x40)          # MIXED (0xFE) is never regular
     code = np.full((m1,) * 3, 0xFF, dtype=np.int64)
     code[pure & ~trac] = smin[pure & ~trac]
@@ -158,7 +163,7 @@ def _row_codes(c, faces):
     return code.reshape(-1)
 
 
-@pytest.mark.parametrize("cfgname,n", [("cfg4", 64), ("cfg2", 64), ("cfg3", 64), ("cfg5", 32)])
+@pytest.mark.parametrize("cfgname,n", [("cfg4", 64), ("cfg2", 64), ("cfg3", 64), ("cfg5", 32), ("cols", 64)])
 def test_classification_and_coarse_classes(cfgname, n):
     """Integer parity, element by element: coarse classes (pure / MIXED, R15) and the
     per-vertex row codes of every level; the coarse coefficient means within 1e-15."""
@@ -183,7 +188,8 @@ def test_classification_and_coarse_classes(cfgname, n):
 
 
 @pytest.mark.parametrize("cfgname,form,mode", [("cfg1", "mod", 0), ("cfg2", "mod", 1),
-                                               ("cfg2", "sym", 1), ("cfg3", "grad", 1)])
+                                               ("cfg2", "sym", 1), ("cfg3", "grad", 1), ("cols", "mod", 0),
+                                               ("cols", "mod", 1), ("cols", "sym", 1)])
 def test_uzawa_step_and_vcycle(cfgname, form, mode):
     n = 16 if mode == 0 else 32
     nc = 4 if form == "sym" else 2
@@ -228,7 +234,8 @@ def test_transfers():
 
 @pytest.mark.parametrize("cfgname,n,form", [("cfg1", 16, "mod"), ("cfg2", 16, "mod"),
                                             ("cfg3", 16, "mod"), ("cfg5", 16, "mod"),
-                                            ("cfg4", 16, "mod"), ("cfg2", 16, "sym"), ("cfg5", 16, "grad")])
+                                            ("cfg4", 16, "mod"), ("cfg2", 16, "sym"), ("cfg5", 16, "grad"),
+                                            ("cols", 16, "mod"), ("cols", 16, "sym"), ("cols", 16, "grad")])
 def test_solve_matches_direct_solution(cfgname, n, form):
     """Converged solve vs the oracle's direct solve (north_star: 1e-8 per field).
     The unresolved high-contrast inclusions (cfg3, cfg5) need the V-cycle as a
@@ -245,7 +252,7 @@ def test_solve_matches_direct_solution(cfgname, n, form):
     assert err <= 1e-8, errs
 
 
-@pytest.mark.parametrize("cfgname,n,kry", [("cfg1", 64, 0), ("cfg2", 64, 0), ("cfg3", 64, 30)])
+@pytest.mark.parametrize("cfgname,n,kry", [("cfg1", 64, 0), ("cfg2", 64, 0), ("cfg3", 64, 30), ("cols", 64, 0)])
 def test_solve_on_tiled_levels_matches_oracle_multigrid(cfgname, n, kry):
     """Converged solve at sizes where the tiled (TMA) kernels run (n >= 64) against
     the oracle multigrid with element-loop products solved to 1e-13 (plain V-cycles,
@@ -294,7 +301,7 @@ def test_solve_cfg1_rate():
 
 @pytest.mark.parametrize("cfgname,n,form", [("cfg2", 64, "mod"), ("cfg3", 64, "grad"),
                                             ("cfg2", 64, "sym"), ("cfg5", 128, "mod"),
-                                            ("cfg4", 128, "mod")])
+                                            ("cfg4", 128, "mod"), ("cols", 64, "mod"), ("cols", 128, "mod")])
 def test_tiled_smoother_and_vcycle_vs_matrix_free_oracle(cfgname, n, form):
     """Tiled TMA kernels (levels n >= 64) against the oracle multigrid with
     element-loop products (oracle.mg_mf): one Uzawa step, one V-cycle."""
@@ -336,7 +343,7 @@ def test_tiled_equals_generic_device_path():
 
 
 @pytest.mark.parametrize("cfgname,n,form", [("cfg1", 16, "mod"), ("cfg2", 64, "mod"), ("cfg2", 32, "sym"),
-                                            ("cfg3", 64, "grad"), ("cfg5", 64, "mod")])
+                                            ("cfg3", 64, "grad"), ("cfg5", 64, "mod"), ("cols", 64, "mod")])
 def test_coarse_level_kernel_paths_agree(cfgname, n, form):
     """The three device paths of the coarse V-cycle levels agree: the lean row
     kernels (default; explicit stencils on the Gamma rows), the element-row /

@@ -10,6 +10,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 cfg = synth.get_config(name, n=n)
 cls, fcls = synth.element_classes(cfg)
+kry = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 ctx = stk.StokesContext(n, "mod", cfg.faces)
 ctx.set_viscosity(cls, cfg.class_mu)
 ctx.assemble()
@@ -47,7 +48,7 @@ for _ in range(ncyc):
 e1.record()
 torch.cuda.synchronize()
 print(f"  without profiling: {e0.elapsed_time(e1)/ncyc:.3f} ms per V-cycle")
-for rn, fz in ((0, 0), (16, 0), (32, 0), (64, 0)):
+for rn, fz in ((0, 0), (16, 0), (32, 0), (64, 0), (16, 8), (16, 16), (32, 32)):
     ctx.set_row_n(rn)
     ctx.set_fuse_n(fz)
     for _ in range(2):
