@@ -60,8 +60,8 @@ CFG_INDEX = {"cfg1": 0, "cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4, "cols": None
 OP_BYTES = {"apply": 65, "residual": 97, "vel_pass": 40, "p_pass1": 48, "p_pass2": 24, "fwd_sweep": 80}
 # iterations our solver needs at rtol 1e-8 (profiles/r02_convergence_probe_gmres.log), for the
 # reference arm's extrapolation of the oracle solve (the oracle cannot run it in minutes)
-REF_ITS = {"cfg1": 11, "cfg2": 13, "cfg3": 29, "cfg4": 36, "cfg5": 59, "cols": 13}
-DEFAULT_KRYLOV = {"cfg1": 0, "cfg2": 0, "cfg3": 30, "cfg4": 30, "cfg5": 30, "cols": 0}
+REF_ITS = {"cfg1": 11, "cfg2": 13, "cfg3": 31, "cfg4": 36, "cfg5": 59, "cols": 13}
+DEFAULT_KRYLOV = {"cfg1": 0, "cfg2": 0, "cfg3": 12, "cfg4": 30, "cfg5": 30, "cols": 0}  # cfg3: measured best (profiles/r02_bench_cfg3_krylov*.json)
 
 
 def workload_name(name):
@@ -238,6 +238,26 @@ def oracle_apply_sample(cfg, form, reps=1, log=None, slab_planes=8):
             "samples": ts}
 
 
+def oracle_solve_measured(name="cfg1", n=16):
+    """A full oracle solve, timed: the assembled-matrix oracle multigrid (oracle/mg.py,
+    scipy, one host thread for the products) on `name` at n to rtol 1e-8 from x = 0 --
+    the size the oracle finishes in seconds (SURVEY 8(d) "oracle beside it")."""
+    from oracle import fem, mg
+    cfg = synth.get_config(name, n=n)
+    cls, fcls = synth.element_classes(cfg)
+    t0 = time.time()
+    H = mg.Hierarchy(n, cls, cfg.class_mu, cfg.faces, "mod")
+    pr = H.levels[0].prob
+    b = (pr.load_nodal(synth.nodal_forcing(cfg)) if cfg.forcing == "nodal"
+         else pr.load_element(fem.element_force(n, fcls, cfg.force_table)))
+    t1 = time.time()
+    _, hist = H.solve(b, rtol=RTOL, max_cycles=200)
+    t2 = time.time()
+    return {"workload": f"{name} n={n}", "dofs": cfg.dofs, "cycles": len(hist) - 1,
+            "setup_s": round(t1 - t0, 3), "solve_s": round(t2 - t1, 3),
+            "s_per_dof": (t2 - t1) / cfg.dofs, "rel_res": hist[-1]}
+
+
 def oracle_solve_extrapolated(cfg, t_apply, its, krylov):
     """s/DoF of the oracle multigrid solve: `its` V_var cycles (plus one apply per
     GMRES iteration and the residuals) at the measured time per full-grid apply."""
@@ -263,13 +283,14 @@ def run_reference(args, cfg, world, rank):
               f"our solver measured at this config")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s/DoF", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * cfg.dofs * 1e3,
-            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": False, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": workload_name(cfg.name), "n": cfg.n,
                        "dofs": cfg.dofs, "form": args.form, "rtol": RTOL},
             "cpu_baseline": {"value": value, "unit": "s/DoF", "cores": smp["threads"], "kind": "oracle",
                              "sample": sample, "apply_gdof_s_all_threads": round(smp["gdof_all"], 4),
-                             "apply_gdof_s_one_thread": round(smp["gdof_one"], 5)},
+                             "apply_gdof_s_one_thread": round(smp["gdof_one"], 5),
+                             "oracle_solve_measured": oracle_solve_measured()},
             "e2e": {"value": value, "unit": "s/DoF", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "extrapolated": True}
     print(json.dumps(line), flush=True)
@@ -458,6 +479,7 @@ def run_ours(args, cfg, world, rank, local):
                               f"{smp['slab_planes']}-plane slab: {smp['t_one_slab']:.2f} s"),
                    "apply_gdof_s_all_threads": round(smp["gdof_all"], 4),
                    "apply_gdof_s_one_thread": round(smp["gdof_one"], 5),
+                   "oracle_solve_measured": oracle_solve_measured(),
                    "extrapolated": True}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "s/DoF", "cores": os.cpu_count(), "kind": "oracle",
@@ -466,7 +488,7 @@ def run_ours(args, cfg, world, rank, local):
     if rank == 0:
         line = {"metric": METRIC, "value": ms * 1e-3 / dofs, "unit": "s/DoF", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": False, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
                 "config": {"workload": workload_name(cfg.name), "n": cfg.n,
                            "dofs": dofs, "form": args.form, "rtol": RTOL,
@@ -474,7 +496,9 @@ def run_ours(args, cfg, world, rank, local):
                            "step": "assemble + load vector + apply + solve", "l2": "flushed between steps",
                            "parallelism": f"z-slab x{world}"},
                 "solve": {"iterations": rep.cycles, "rho": round(rep.rho, 4), "rel_res": rep.rel_res,
-                          "solve_s": rep.t_total_s, "converged_every_step": converged},
+                          "solve_s": rep.t_total_s, "converged_every_step": converged,
+                          "t_level_s": {"finest": round(rep.t_level_s[0], 5),
+                                        "levels_ge_1": round(rep.t_level_s[1], 5)}},
                 "apply": apply_obj,
                 "roofline": roof,
                 "ops_ms_per_step": ops_ms,
@@ -500,10 +524,19 @@ def main():
     ap.add_argument("--krylov", type=int, default=None)
     ap.add_argument("--max-cycles", type=int, default=300)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the workload's n on every N; weak (SURVEY NEXT-3, the JUQUEEN "
+                         "ladder P:1341-1346): n = n_1 * N^(1/3) with n_1 = --n (default 512), N a cube")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    cfg = synth.get_config(args.workload, n=args.n)
     world, rank, local = dist_setup(args)
+    n = args.n
+    if args.scaling == "weak":
+        c = round(world ** (1.0 / 3.0))
+        if c ** 3 != world:
+            raise SystemExit(f"--scaling weak needs a cube number of GPUs (1, 8, 64), got {world}")
+        n = (args.n or 512) * c
+    cfg = synth.get_config(args.workload, n=n)
     if args.impl == "reference":
         rc = run_reference(args, cfg, world, rank)
     else:

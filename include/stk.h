@@ -90,7 +90,14 @@ typedef struct {
                          GMRES(m) with one V-cycle as preconditioner */
   int32_t rank, nranks; /* z-slab owner and number of ranks (one GPU each) */
   void* stream;       /* cudaStream_t; NULL = legacy default stream */
+  int32_t coarse_mu;  /* coarse-level viscosity of the A block per coarse tet, from its 8 Bey
+                         children (DESIGN R15): 0 = default = 1; 1 = arithmetic mean
+                         (the coarse A is then the Galerkin product P^T A P); 2 = harmonic mean.
+                         The weight 1/mu of C and of the gauge is always the mean of the children's
+                         1/mu.  (SURVEY's "centroid" rule is degenerate for Bey refinement: the
+                         coarse centroid lies on the diagonal shared by the four inner children.) */
 } stk_config;
+enum { STK_COARSE_MU_DEFAULT = 0, STK_COARSE_MU_ARITH = 1, STK_COARSE_MU_HARMONIC = 2 };
 
 typedef struct {
   int32_t n;          /* intervals of this level */
@@ -109,6 +116,9 @@ typedef struct {
   double rel_res;     /* ||b - K x|| / ||b|| over free DoFs */
   double t_total_s;   /* device time of the solve */
   double res_hist[256];
+  double t_level_s[16]; /* device time by level: [0] the finest level (smoothing, residual,
+                           transfers to/from level 1, Krylov vector work), [1] levels >= 1
+                           together (one CUDA graph per V-cycle, events around it); rest 0 */
   int32_t nan_seen;
 } stk_report;
 

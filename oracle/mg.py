@@ -124,11 +124,15 @@ def child_parent(nf: int) -> np.ndarray:
     return out
 
 
-def coarse_viscosity(nf: int, mu_a: np.ndarray, imu_c: np.ndarray):
-    """Coarse per-element (mu_A, 1/mu_C): means over the 8 Bey children (reading R15)."""
+def coarse_viscosity(nf: int, mu_a: np.ndarray, imu_c: np.ndarray, mode: str = "arith"):
+    """Coarse per-element (mu_A, 1/mu_C): means over the 8 Bey children (reading R15);
+    mode "harmonic": mu_A = 8 / sum 1/mu_A (stk_config.coarse_mu = 2)."""
     par = child_parent(nf)
     E = 6 * (nf // 2) ** 3
-    mu_c = np.bincount(par, weights=np.asarray(mu_a, dtype=np.float64).reshape(-1), minlength=E) / 8.0
+    if mode == "harmonic":
+        mu_c = 8.0 / np.bincount(par, weights=1.0 / np.asarray(mu_a, dtype=np.float64).reshape(-1), minlength=E)
+    else:
+        mu_c = np.bincount(par, weights=np.asarray(mu_a, dtype=np.float64).reshape(-1), minlength=E) / 8.0
     imu_cc = np.bincount(par, weights=np.asarray(imu_c, dtype=np.float64).reshape(-1), minlength=E) / 8.0
     return mu_c, imu_cc
 
@@ -162,7 +166,7 @@ class Level:
 class Hierarchy:
     def __init__(self, n, cls, class_mu, faces, form="mod", delta=1.0 / 12.0,
                  n_coarse=4, nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2,
-                 coarse="direct", minres_its=20, cg_its=4):
+                 coarse="direct", minres_its=20, cg_its=4, coarse_mu="arith"):
         self.levels = []
         self.P = []
         c = np.asarray(cls, dtype=np.uint8)
@@ -175,7 +179,7 @@ class Hierarchy:
                 break
             assert m % 2 == 0
             self.P.append(prolongation(m // 2))
-            mu_a, imu_c = coarse_viscosity(m, mu_a, imu_c)
+            mu_a, imu_c = coarse_viscosity(m, mu_a, imu_c, coarse_mu)
             c = coarse_classes(m, c)
             m //= 2
         self.nu_pre, self.nu_post, self.nu_inc = nu_pre, nu_post, nu_inc

@@ -95,7 +95,7 @@ class MFLevel:
 class MFHierarchy(mg.Hierarchy):
     def __init__(self, n, cls, class_mu, faces, form="mod", delta=1.0 / 12.0,
                  n_coarse=4, nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2,
-                 coarse="direct", minres_its=20, cg_its=4):
+                 coarse="direct", minres_its=20, cg_its=4, coarse_mu="arith"):
         self.levels, self.P = [], []
         c = np.asarray(cls, dtype=np.uint8)
         mu_a = np.asarray(class_mu, dtype=np.float64)[c]
@@ -106,7 +106,7 @@ class MFHierarchy(mg.Hierarchy):
             if m <= n_coarse:
                 break
             self.P.append(mg.prolongation(m // 2))
-            mu_a, imu_c = mg.coarse_viscosity(m, mu_a, imu_c)
+            mu_a, imu_c = mg.coarse_viscosity(m, mu_a, imu_c, coarse_mu)
             c = mg.coarse_classes(m, c)
             m //= 2
         self.nu_pre, self.nu_post, self.nu_inc = nu_pre, nu_post, nu_inc

@@ -37,7 +37,8 @@ class stk_config(ctypes.Structure):
                 ("face", ctypes.c_int32 * 6), ("delta", ctypes.c_double),
                 ("nu_pre", ctypes.c_int32), ("nu_post", ctypes.c_int32), ("nu_inc", ctypes.c_int32),
                 ("omega", ctypes.c_double), ("ncolors_u", ctypes.c_int32), ("krylov", ctypes.c_int32),
-                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("stream", ctypes.c_void_p)]
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("stream", ctypes.c_void_p),
+                ("coarse_mu", ctypes.c_int32)]
 
 
 class stk_layout_t(ctypes.Structure):
@@ -51,7 +52,7 @@ class stk_layout_t(ctypes.Structure):
 class stk_report(ctypes.Structure):
     _fields_ = [("cycles", ctypes.c_int32), ("rho", ctypes.c_double), ("rel_res", ctypes.c_double),
                 ("t_total_s", ctypes.c_double), ("res_hist", ctypes.c_double * 256),
-                ("nan_seen", ctypes.c_int32)]
+                ("t_level_s", ctypes.c_double * 16), ("nan_seen", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p
@@ -169,7 +170,8 @@ class StokesContext:
 
     def __init__(self, n, form="mod", faces=(0,) * 6, delta=1.0 / 12.0, n_coarse=4,
                  nu_pre=3, nu_post=3, nu_inc=2, omega=0.3, ncolors_u=2, krylov=0, rank=0, nranks=1,
-                 stream=None, nccl_id: bytes | None = None, loopback: LoopbackGroup | None = None):
+                 stream=None, nccl_id: bytes | None = None, loopback: LoopbackGroup | None = None,
+                 coarse_mu="arith"):
         import torch
         self.torch = torch
         cfg = stk_config()
@@ -179,6 +181,7 @@ class StokesContext:
         cfg.delta, cfg.nu_pre, cfg.nu_post, cfg.nu_inc = delta, nu_pre, nu_post, nu_inc
         cfg.omega, cfg.ncolors_u, cfg.rank, cfg.nranks = omega, ncolors_u, rank, nranks
         cfg.krylov = krylov
+        cfg.coarse_mu = {"arith": 1, "harmonic": 2}[coarse_mu]
         if stream is None:
             stream = torch.cuda.current_stream()
         self.stream = stream

@@ -315,7 +315,7 @@ __global__ void k_unpack(DGrid g, const double* __restrict__ dev, double* __rest
 // of the children's 1/mu_C; the class is the children's common class, else CLS_MIXED.
 // gf/gc: fine/coarse grids (cube layers stored); cls_c / emu_c in gc's layout.
 __global__ void k_coarsen(DGrid gf, DGrid gc, int CK0, int CK1, uint8_t* __restrict__ cls_c,
-                          double2* __restrict__ emu_c) {
+                          double2* __restrict__ emu_c, int harmonic) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int nc = gc.n;
   const int64_t total = (int64_t)(CK1 - CK0) * nc * nc * 6;
@@ -336,14 +336,16 @@ __global__ void k_coarsen(DGrid gf, DGrid gc, int CK0, int CK1, uint8_t* __restr
     const int cl = elem_class(gf, fi, fj, fk, ft);
     double mu, imu;
     tet_coef(gf, fi, fj, fk, ft, cl, mu, imu);
-    sm += mu;
+    sm += harmonic ? 1.0 / mu : mu;
     si += imu;
     if (q == 0) c0 = cl;
     pure = pure && cl == c0 && cl != CLS_MIXED;
   }
   const int64_t o = elem_index(gc, CI, CJ, CK, T);
   cls_c[o] = pure ? (uint8_t)c0 : CLS_MIXED;
-  emu_c[o] = make_double2(sm * 0.125, si * 0.125);
+  // mu_A: arithmetic mean of the 8 children (R15; the Galerkin product), or harmonic
+  // (coarse_mu = 2); 1/mu_C: arithmetic mean of the children's 1/mu_C
+  emu_c[o] = make_double2(harmonic ? 8.0 / sm : sm * 0.125, si * 0.125);
 }
 
 // number of entries >= lim (input validation of the element classes)
@@ -466,71 +468,6 @@ __global__ void k_coarse_assemble(DGrid g, const int32_t* __restrict__ dofs, int
   K[(int64_t)r * N1 + c] = v;
 }
 
-// In-place Gauss-Jordan inverse with partial pivoting of an N x N matrix (one block).
-__global__ void k_gauss_jordan(double* __restrict__ A, double* __restrict__ Inv, int N,
-                               int* __restrict__ status) {
-  __shared__ int piv;
-  __shared__ double redv[1024];
-  __shared__ int redi[1024];
-  for (int64_t e = threadIdx.x; e < (int64_t)N * N; e += blockDim.x)
-    Inv[e] = (e / N == e % N) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int c = 0; c < N; ++c) {
-    double best = -1.0;
-    int bi = c;
-    for (int r = c + threadIdx.x; r < N; r += blockDim.x) {
-      const double v = fabs(A[(int64_t)r * N + c]);
-      if (v > best) { best = v; bi = r; }
-    }
-    redv[threadIdx.x] = best;
-    redi[threadIdx.x] = bi;
-    __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-      if (threadIdx.x < s && (redv[threadIdx.x + s] > redv[threadIdx.x] ||
-                              (redv[threadIdx.x + s] == redv[threadIdx.x] &&
-                               redi[threadIdx.x + s] < redi[threadIdx.x]))) {
-        redv[threadIdx.x] = redv[threadIdx.x + s];
-        redi[threadIdx.x] = redi[threadIdx.x + s];
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      piv = redi[0];
-      if (!(redv[0] > 0.0)) *status = 1;
-    }
-    __syncthreads();
-    const int p = piv;
-    if (p != c) {
-      for (int q = threadIdx.x; q < N; q += blockDim.x) {
-        double t = A[(int64_t)c * N + q]; A[(int64_t)c * N + q] = A[(int64_t)p * N + q]; A[(int64_t)p * N + q] = t;
-        t = Inv[(int64_t)c * N + q]; Inv[(int64_t)c * N + q] = Inv[(int64_t)p * N + q]; Inv[(int64_t)p * N + q] = t;
-      }
-    }
-    __syncthreads();
-    const double d = A[(int64_t)c * N + c];
-    __syncthreads();
-    for (int q = threadIdx.x; q < N; q += blockDim.x) {
-      A[(int64_t)c * N + q] /= d;
-      Inv[(int64_t)c * N + q] /= d;
-    }
-    __syncthreads();
-    for (int64_t e = threadIdx.x; e < (int64_t)N * N; e += blockDim.x) {
-      const int r = (int)(e / N), q = (int)(e % N);
-      if (r == c || q == c) continue;
-      const double fct = A[(int64_t)r * N + c];
-      A[e] -= fct * A[(int64_t)c * N + q];
-      Inv[e] -= fct * Inv[(int64_t)c * N + q];
-    }
-    __syncthreads();
-    for (int r = threadIdx.x; r < N; r += blockDim.x) {
-      if (r == c) continue;
-      const double fct = A[(int64_t)r * N + c];
-      Inv[(int64_t)r * N + c] -= fct * Inv[(int64_t)c * N + c];
-      A[(int64_t)r * N + c] = 0.0;
-    }
-    __syncthreads();
-  }
-}
 
 // x_F = G b_F on the coarsest level (G: N x N with leading dimension ld); other entries 0
 __global__ void k_coarse_apply(DGrid g, const int32_t* __restrict__ dofs, int N, int ld,

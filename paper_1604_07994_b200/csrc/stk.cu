@@ -134,6 +134,8 @@ struct stk_ctx {
   int nparts = 0;
   Comm comm;
   Prof prof;
+  Prof lvl_pool;          // events around the coarse part of each V-cycle (stk_report.t_level_s)
+  int lvl_timing = 0;
   // Krylov workspace (GMRES(m), cfg.krylov = m)
   double* kbasis = nullptr;  // (m+1) level-0 vectors
   double* kwork = nullptr;   // 3 level-0 vectors: w, z, r
@@ -792,7 +794,18 @@ stk_status op_fused(stk_ctx* ctx) {
 // levels only touch context-owned buffers, so the whole sequence (a few hundred
 // small launches with the V_var schedule) is captured once into a CUDA graph
 // and replayed; the graph is rebuilt after every stk_assemble.
+stk_status op_coarse_part_impl(stk_ctx* ctx);
+// levels >= 1 of the V-cycle, bracketed by events while stk_solve collects t_level_s
 stk_status op_coarse_part(stk_ctx* ctx) {
+  if (!ctx->lvl_timing) return op_coarse_part_impl(ctx);
+  cudaEvent_t e0 = ctx->lvl_pool.get(), e1 = ctx->lvl_pool.get();
+  CK(cudaEventRecord(e0, ctx->stream));
+  const stk_status s = op_coarse_part_impl(ctx);
+  CK(cudaEventRecord(e1, ctx->stream));
+  ctx->lvl_pool.recs.push_back({P_CGRAPH, 1, e0, e1});
+  return s;
+}
+stk_status op_coarse_part_impl(stk_ctx* ctx) {
   Level& C = ctx->lev[1];
   static const bool no_graph = getenv("STK_NO_GRAPH") && atoi(getenv("STK_NO_GRAPH"));
   if (ctx->fl == 1) return op_fused(ctx);  // one launch: nothing to capture
@@ -1298,6 +1311,7 @@ stk_status create_impl(const stk_config* cfg, const uint8_t* id, stk_loopback* g
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return STK_EINVAL;
   if (cfg->ncolors_u != 2 && cfg->ncolors_u != 4) return STK_EINVAL;
   if (cfg->krylov < 0 || cfg->krylov > 200) return STK_EINVAL;
+  if (cfg->coarse_mu < 0 || cfg->coarse_mu > 2) return STK_EINVAL;
   const int nc = cfg->n_coarse > 0 ? cfg->n_coarse : 4;
   if (nc > n || (nc & (nc - 1)) != 0 || nc > 16) return STK_EINVAL;
   bool any_dir = false, slip_axis[3] = {false, false, false};
@@ -1453,7 +1467,8 @@ stk_status stk_assemble(stk_ctx* ctx) {
     auto coarsen = [&](int CK0, int CK1) -> stk_status {
       const int64_t tot = (int64_t)(CK1 - CK0) * lay;
       if (tot <= 0) return STK_OK;
-      k_coarsen<<<nblocks(tot), kThreads, 0, ctx->stream>>>(dgrid(ctx, F), dgrid(ctx, C), CK0, CK1, C.cls, C.emu);
+      k_coarsen<<<nblocks(tot), kThreads, 0, ctx->stream>>>(dgrid(ctx, F), dgrid(ctx, C), CK0, CK1, C.cls, C.emu,
+                                                            ctx->cfg.coarse_mu == STK_COARSE_MU_HARMONIC);
       return launched(ctx);
     };
     if (C.replicated && !F.replicated) {
@@ -1868,6 +1883,8 @@ stk_status stk_solve(stk_ctx* ctx, const double* b, double* x, double rtol, int3
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, ctx->stream));
+  ctx->lvl_pool.reset();
+  ctx->lvl_timing = ctx->nlev > 1;
   double nb[5];
   ST(stk_norms(ctx, 0, b, nb));
   const double bnorm = std::sqrt(nb[4]);
@@ -1892,6 +1909,7 @@ stk_status stk_solve(stk_ctx* ctx, const double* b, double* x, double rtol, int3
       }
     }
   }
+  ctx->lvl_timing = 0;
   ST(op_gauge(ctx, 0, x));
   CK(cudaEventRecord(e1, ctx->stream));
   CK(cudaEventSynchronize(e1));
@@ -1899,6 +1917,15 @@ stk_status stk_solve(stk_ctx* ctx, const double* b, double* x, double rtol, int3
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  double coarse_ms = 0.0;
+  for (auto& r : ctx->lvl_pool.recs) {
+    float t = 0;
+    cudaEventElapsedTime(&t, r.e0, r.e1);
+    coarse_ms += t;
+  }
+  ctx->lvl_pool.reset();
+  R->t_level_s[0] = (ms - coarse_ms) * 1e-3;
+  R->t_level_s[1] = coarse_ms * 1e-3;
   R->cycles = cyc;
   R->rel_res = rel;
   R->t_total_s = ms * 1e-3;
@@ -2047,6 +2074,7 @@ stk_status stk_destroy(stk_ctx* ctx) {
   cudaFreeHost(ctx->hsums);
   ctx->comm.destroy();
   ctx->prof.destroy();
+  ctx->lvl_pool.destroy();
   cudaFree(ctx->kbasis);
   cudaFree(ctx->kwork);
   cudaFree(ctx->kz);

@@ -163,11 +163,13 @@ def _row_codes(c, faces):
     return code.reshape(-1)
 
 
-@pytest.mark.parametrize("cfgname,n", [("cfg4", 64), ("cfg2", 64), ("cfg3", 64), ("cfg5", 32), ("cols", 64)])
-def test_classification_and_coarse_classes(cfgname, n):
+@pytest.mark.parametrize("cfgname,n,cmu", [("cfg4", 64, "arith"), ("cfg2", 64, "arith"), ("cfg3", 64, "arith"),
+                                           ("cfg5", 32, "arith"), ("cols", 64, "arith"), ("cfg3", 64, "harmonic")])
+def test_classification_and_coarse_classes(cfgname, n, cmu):
     """Integer parity, element by element: coarse classes (pure / MIXED, R15) and the
-    per-vertex row codes of every level; the coarse coefficient means within 1e-15."""
-    ctx, cfg, cls, _ = make_ctx(cfgname, n, "mod")
+    per-vertex row codes of every level; the coarse coefficient means within 1e-15
+    (stk_config.coarse_mu: arithmetic, or harmonic for the A block)."""
+    ctx, cfg, cls, _ = make_ctx(cfgname, n, "mod", coarse_mu=cmu)
     c = np.asarray(cls, dtype=np.uint8)
     mu_a = np.asarray(cfg.class_mu, dtype=np.float64)[c]
     imu_c = 1.0 / mu_a
@@ -182,19 +184,20 @@ def test_classification_and_coarse_classes(cfgname, n):
         np.testing.assert_array_equal(ctx.export_codes(l).astype(np.int64), want)
         assert ctx.layout(l).n_irregular == int((want == 0xFF).sum())
         if l + 1 < ctx.nlev:   # the oracle's coarse level (R15)
-            mu_a, imu_c = mg.coarse_viscosity(m, mu_a, imu_c)
+            mu_a, imu_c = mg.coarse_viscosity(m, mu_a, imu_c, cmu)
             c = mg.coarse_classes(m, c)
             m //= 2
 
 
-@pytest.mark.parametrize("cfgname,form,mode", [("cfg1", "mod", 0), ("cfg2", "mod", 1),
-                                               ("cfg2", "sym", 1), ("cfg3", "grad", 1), ("cols", "mod", 0),
-                                               ("cols", "mod", 1), ("cols", "sym", 1)])
-def test_uzawa_step_and_vcycle(cfgname, form, mode):
+@pytest.mark.parametrize("cfgname,form,mode,cmu", [("cfg1", "mod", 0, "arith"), ("cfg2", "mod", 1, "arith"),
+                                                   ("cfg2", "sym", 1, "arith"), ("cfg3", "grad", 1, "arith"),
+                                                   ("cols", "mod", 0, "arith"), ("cols", "mod", 1, "arith"),
+                                                   ("cols", "sym", 1, "arith"), ("cfg3", "mod", 1, "harmonic")])
+def test_uzawa_step_and_vcycle(cfgname, form, mode, cmu):
     n = 16 if mode == 0 else 32
     nc = 4 if form == "sym" else 2
-    ctx, cfg, cls, fcls = make_ctx(cfgname, n, form, kernel_mode=mode, ncolors_u=nc)
-    h = mg.Hierarchy(n, cls, cfg.class_mu, cfg.faces, form=form, ncolors_u=nc)
+    ctx, cfg, cls, fcls = make_ctx(cfgname, n, form, kernel_mode=mode, ncolors_u=nc, coarse_mu=cmu)
+    h = mg.Hierarchy(n, cls, cfg.class_mu, cfg.faces, form=form, ncolors_u=nc, coarse_mu=cmu)
     pr = h.levels[0].prob
     rng = np.random.default_rng(3)
     x = np.where(pr.free, rng.uniform(-1, 1, 4 * pr.V), 0.0)

@@ -299,6 +299,7 @@ def test_coarse_viscosity_and_class_brute_force():
     cls[:6 * nf * nf] = 1                  # a layer of pure coarse tets too
     mu = np.array([1.0, 7.0, 3.0])
     mu_a, imu_c = mg.coarse_viscosity(nf, mu[cls], 1.0 / mu[cls])
+    mu_h, imu_h = mg.coarse_viscosity(nf, mu[cls], 1.0 / mu[cls], "harmonic")
     cc = mg.coarse_classes(nf, cls)
     seen_mixed = seen_pure = False
     for K, J, I, T in itertools.product(range(2), range(2), range(2), range(6)):
@@ -307,6 +308,9 @@ def test_coarse_viscosity_and_class_brute_force():
         e = ((K * 2 + J) * 2 + I) * 6 + T
         assert mu_a[e] == pytest.approx(np.mean(mu[cls[ch]]), rel=1e-15)
         assert imu_c[e] == pytest.approx(np.mean(1.0 / mu[cls[ch]]), rel=1e-15)
+        # stk_config.coarse_mu = 2: harmonic mean for A, the same 1/mu_C
+        assert mu_h[e] == pytest.approx(8.0 / np.sum(1.0 / mu[cls[ch]]), rel=1e-15)
+        assert imu_h[e] == imu_c[e]
         if len(set(cls[ch])) == 1:
             assert cc[e] == cls[ch[0]]
             seen_pure = True
