@@ -570,7 +570,30 @@ stk_status op_coarse_minres(stk_ctx* ctx, const double* b, double* x) {
   A.its = ctx->mr_its;
   A.cg_its = ctx->mr_cg;
   PScope ps(ctx, P_COARSE, ctx->nlev - 1);
-  k_coarse_minres<FORM_SYM><<<1, MR_NT, 0, ctx->stream>>>(A);
+  const int64_t V = owned_vertices(L);
+  // one cluster: 1 CTA (n_c = 4), 8 (n_c = 8), 16 (n_c = 16, non-portable size)
+  const int cl = V <= 256 ? 1 : V <= 1500 ? 8 : 16;
+  if (cl == 1) {
+    k_coarse_minres<FORM_SYM, 1><<<1, MR_NT, 0, ctx->stream>>>(A);
+    return launched(ctx);
+  }
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(cl);
+  lc.blockDim = dim3(MR_NT);
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  if (cl == 8) {
+    CK(cudaLaunchKernelEx(&lc, k_coarse_minres<FORM_SYM, 8>, A));
+  } else {
+    CK(cudaFuncSetAttribute(k_coarse_minres<FORM_SYM, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaLaunchKernelEx(&lc, k_coarse_minres<FORM_SYM, 16>, A));
+  }
   return launched(ctx);
 }
 

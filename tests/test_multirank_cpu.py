@@ -68,14 +68,14 @@ def test_partition_owns_every_plane_once(n, P):
             assert np.all(cover == 1)
 
 
-def _worker(rank, world, port, n, q):
+def _worker(rank, world, port, n, q, cfgname="cfg4"):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        cfg = synth.get_config("cfg4", n=n)
+        cfg = synth.get_config(cfgname, n=n)
         cls, _ = synth.element_classes(cfg)
         x = synth.apply_input(cfg)                       # (4, V) global, same seed on every rank
         N1 = n + 1
@@ -120,21 +120,21 @@ def _worker(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_slab_apply_with_gloo_halo_exchange_equals_global_oracle(world):
+@pytest.mark.parametrize("world,cfgname", [(2, "cfg4"), (2, "cols")])
+def test_slab_apply_with_gloo_halo_exchange_equals_global_oracle(world, cfgname):
     import torch.multiprocessing as mp
     n = 16
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q, cfgname)) for r in range(world)]
     for p in procs:
         p.start()
     gathered, nrm = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    cfg = synth.get_config("cfg4", n=n)
+    cfg = synth.get_config(cfgname, n=n)
     cls, _ = synth.element_classes(cfg)
     x = synth.apply_input(cfg)
     N1 = n + 1
