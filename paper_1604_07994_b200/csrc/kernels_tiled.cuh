@@ -527,11 +527,14 @@ __global__ void __launch_bounds__(LX_NT) k_listx(DGrid g, StreamArgs a, const do
   if (OP == OP_VEL) act = ((i + j + k) & (a.ncolors - 1)) == a.color && em != 7u;
   if (OP == OP_P2) act = !c0;
   double py[4] = {0.0, 0.0, 0.0, 0.0};
-  if (act && q < NQ) {
-    const int dx = kq_dx(q), dy = kq_dy(q), dz = kq_dz(q);
-    const int xi = i + dx, yj = j + dy, zk = k + dz;
+  // lanes of out-of-cube neighbours contribute 0 (their inputs are 0): they skip the
+  // stencil loads, as do the rows of eliminated components (zero rows) -- boundary rows
+  // of the free-slip / Dirichlet faces read a quarter to a half fewer stencil bytes
+  const int dx = q < NQ ? kq_dx(q) : 0, dy = q < NQ ? kq_dy(q) : 0, dz = q < NQ ? kq_dz(q) : 0;
+  const int xi = i + dx, yj = j + dy, zk = k + dz;
+  const bool in = xi >= 0 && yj >= 0 && zk >= 0 && xi <= g.n && yj <= g.n && zk <= g.n;
+  if (act && q < NQ && in) {
     const int n = g.n;
-    const bool in = xi >= 0 && yj >= 0 && zk >= 0 && xi <= n && yj <= n && zk <= n;
     const int64_t oc = o + dx + dy * g.px + dz * g.py;
     double u[3] = {0.0, 0.0, 0.0}, p = 0.0;
     if (UCOL) {
@@ -550,6 +553,7 @@ __global__ void __launch_bounds__(LX_NT) k_listx(DGrid g, StreamArgs a, const do
     if (VROWS) {
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
+        if ((em >> r) & 1u) continue;  // eliminated component: zero row
         const double2 s01 = __ldg(reinterpret_cast<const double2*>(S + (r * NQ + q) * 4));
         const double2 s23 = __ldg(reinterpret_cast<const double2*>(S + (r * NQ + q) * 4 + 2));
         const bool wA = OP == OP_VEL || OP == OP_RESID || (a.blocks & BLK_A);

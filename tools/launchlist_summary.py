@@ -17,7 +17,8 @@ for r in csv.DictReader(lines):
         continue
     v = float(r["Metric Value"].replace(",", ""))
     unit = r.get("Metric Unit", "")
-    us = v * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
+    us = v * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+              "second": 1e6, "s": 1e6}[unit]
     rows.append((r["Kernel Name"], us))
 agg = collections.defaultdict(lambda: [0, 0.0])
 for k, us in rows:

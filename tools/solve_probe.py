@@ -17,3 +17,6 @@ b = ctx.load_nodal(synth.nodal_forcing(cfg)) if cfg.forcing == "nodal" else ctx.
 x, rep = ctx.solve(b, rtol=1e-8, max_cycles=200)
 h = [rep.res_hist[i] for i in range(min(rep.cycles, 256))]
 print(f"{name} n={n} krylov={kry} coarse_mu={cmu} n_coarse={nc}: its={rep.cycles} rel={rep.rel_res:.3e} t={rep.t_total_s:.3f}s hist[0:8]={np.array(h[:8])} last={h[-3:]}")
+r, nr = ctx.residual(x, b, norms=True)
+nb = ctx.norms(b)
+print(f"  residual per field (u1,u2,u3,p): {np.sqrt(nr[:4])}  |b| per field: {np.sqrt(nb[:4])}")
