@@ -60,8 +60,11 @@ CFG_INDEX = {"cfg1": 0, "cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4, "cols": None
 OP_BYTES = {"apply": 65, "residual": 97, "vel_pass": 40, "p_pass1": 48, "p_pass2": 24, "fwd_sweep": 80}
 # iterations our solver needs at rtol 1e-8 (profiles/r02_convergence_probe_gmres.log), for the
 # reference arm's extrapolation of the oracle solve (the oracle cannot run it in minutes)
-REF_ITS = {"cfg1": 11, "cfg2": 13, "cfg3": 31, "cfg4": 36, "cfg5": 59, "cols": 13}
-DEFAULT_KRYLOV = {"cfg1": 0, "cfg2": 0, "cfg3": 12, "cfg4": 30, "cfg5": 30, "cols": 0}  # cfg3: measured best (profiles/r02_bench_cfg3_krylov*.json)
+REF_ITS = {"cfg1": 11, "cfg2": 13, "cfg3": 31, "cfg4": 100, "cfg5": 59, "cols": 13}
+DEFAULT_KRYLOV = {"cfg1": 0, "cfg2": 0, "cfg3": 12, "cfg4": 100, "cfg5": 30, "cols": 0}
+# cfg3: measured best (profiles/r02_bench_cfg3_krylov*.json); cfg5: 30 (12 doubles the iterations);
+# cfg4: the plain V-cycle diverges (rho ~ 7 at n = 256) and GMRES(30) stagnates at 5e-4 --
+# GMRES(100) converges in 100 iterations (profiles/r02_cfg4_n256_probe.log)
 
 
 def workload_name(name):
