@@ -28,8 +28,10 @@
  *    column i = -1 and row j = -1 are an unused ghost frame).
  *    Allocate stk_layout(...).vec_len doubles per vector.
  *  - Velocity entries at Dirichlet vertices (closure of Dirichlet faces) are
- *    ignored on input (treated as 0) and written as 0 on output.  Pressure
- *    lives at every vertex.
+ *    ignored on input (treated as 0) and written as 0 on output.  On free-slip
+ *    faces the normal component is eliminated: it is written as 0 on output and
+ *    must be 0 on input (stk_zero_eliminated; every library output keeps it).
+ *    Pressure lives at every vertex.
  *  - All device work is stream-ordered on cfg.stream; calls return before the
  *    work completes, except stk_solve and calls that return host data.
  *  - Errors: STK_EINVAL bad argument / size; STK_ESTATE call order violated
@@ -210,13 +212,23 @@ stk_status stk_residual(stk_ctx* ctx, int32_t level, const double* x, const doub
 stk_status stk_smooth(stk_ctx* ctx, int32_t level, double* x, const double* b, int32_t steps);
 /* b_c = R r_f = P^T r_f, coarse level = fine_level + 1 */
 stk_status stk_restrict(stk_ctx* ctx, int32_t fine_level, const double* r_f, double* b_c);
-/* x_f += P x_c (linear interpolation on coarse Kuhn edges) */
+/* x_f += P x_c: the "standard" prolongation of P:1243 (DESIGN R14) -- nodal
+ * interpolation of the coarse P1 function (fine vertex 2I takes x_c(I), the midpoint
+ * of the coarse Kuhn edge (I, I+d) the mean of its ends), all 4 fields; eliminated
+ * velocity entries of x_f stay 0.  coarse_level = fine level + 1; x_c needs no halo. */
 stk_status stk_prolong_add(stk_ctx* ctx, int32_t coarse_level, const double* x_c, double* x_f);
-/* one V_var cycle on the finest level, in place on x */
+/* one V_var cycle (nu_pre + nu_inc*l Uzawa steps before and
+ * nu_post + nu_inc*l after the coarse correction on level l, restriction R = P^T,
+ * coarsest-level solve as stk_set_coarse_solver selects) on the finest level, in
+ * place on x; b and x are finest-level device vectors. */
 stk_status stk_vcycle(stk_ctx* ctx, const double* b, double* x);
-/* V-cycles (or GMRES iterations, cfg.krylov > 0; max_cycles bounds the number of
- * preconditioner applications) until ||b-Kx||/||b|| <= rtol (synchronous);
- * gauge applied at the end */
+/* Solve K x = b from the given x: V_var cycles (the paper's
+ * all-at-once multigrid) or, cfg.krylov = m > 0, right-preconditioned GMRES(m) with
+ * one V-cycle from zero as the preconditioner (DESIGN R23), until ||b - Kx||/||b|| <=
+ * rtol over the free DoFs; max_cycles bounds the preconditioner applications.  The
+ * mu^-1-weighted pressure gauge is applied at the end.  Synchronous; report
+ * (may be NULL) gets the residual history, rho, device time and t_level_s.
+ * STK_ENOCONV (positive: x holds the last iterate) when rtol is not reached. */
 stk_status stk_solve(stk_ctx* ctx, const double* b, double* x, double rtol, int32_t max_cycles,
                      stk_report* report);
 /* subtract the mu^-1-weighted mean pressure (Q of P:136); no-op with traction faces */

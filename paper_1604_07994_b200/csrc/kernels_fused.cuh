@@ -750,6 +750,7 @@ __global__ void __launch_bounds__(ROW_NT) k_rowl(const __grid_constant__ FLevel 
 
 // ---- fused persistent V-cycle (optional, stk_set_fuse_n) ------------------------
 constexpr int FMAX = 8;
+constexpr int FCL = 16;  // CTAs of the fused V-cycle's thread-block cluster (non-portable size)
 // one phase of the fused V-cycle (built on the host, read from shared memory)
 struct FPhase {
   uint8_t op, lev, color, flip;  // flip (FPH_VEL): input in the scratch vector, output in x
@@ -770,6 +771,7 @@ struct FusedArgs {
   int cN, cld;
   unsigned long long* bar;
   unsigned long long* trace;  // debug (STK_FUSED_TRACE): globaltimer after every phase, CTA 0
+  int cluster;                // 1: the grid is one thread-block cluster, phases end at a cluster barrier
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -812,7 +814,11 @@ __global__ void __launch_bounds__(256, 1) k_mg_fused(const __grid_constant__ Fus
         default: f_coarse<true>(L, A.cdofs, A.cG, A.cN, A.cld, t0 >> 5, nthr >> 5); break;
       }
     }
-    if (P.barM > 0 && (int)blockIdx.x < P.barM) grid_barrier(A.bar, P.barM);
+    if (A.cluster) {
+      cooperative_groups::this_cluster().sync();  // hardware barrier; release/acquire at cluster scope
+    } else if (P.barM > 0 && (int)blockIdx.x < P.barM) {
+      grid_barrier(A.bar, P.barM);
+    }
     if (tr) A.trace[ph] = globaltimer();
   }
 }

@@ -125,6 +125,7 @@ struct stk_ctx {
   std::vector<int64_t> graph_sig;         // what the captured coarse graph depends on
   FPhase* fprog = nullptr;                // phase program of the fused V-cycle (device)
   int fnph = 0, fgrid_used = 0;
+  int fcluster = 1;  // fused V-cycle on one 16-CTA thread-block cluster (cluster barriers) when it fits
   double* cfac = nullptr;                 // Gauss-Jordan column factors
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // reductions
@@ -769,12 +770,21 @@ stk_status launch_fused_t(stk_ctx* ctx) {
   A.cld = ctx->cN1;
   A.bar = ctx->fbar;
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(ctx->fgrid_used);
+  A.cluster = ctx->fcluster;
+  lc.gridDim = dim3(ctx->fcluster ? FCL : ctx->fgrid_used);
   lc.blockDim = dim3(256);
   lc.stream = ctx->stream;
   cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
+  if (ctx->fcluster) {
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = FCL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    CK(cudaFuncSetAttribute(k_mg_fused<FORM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  } else {
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+  }
   lc.attrs = at;
   lc.numAttrs = 1;
   static const bool trace = getenv("STK_FUSED_TRACE") && atoi(getenv("STK_FUSED_TRACE"));
@@ -1117,6 +1127,8 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
 
 // persistent-grid size (one 256-thread CTA per SM) and the barrier words
 stk_status fused_setup(stk_ctx* ctx) {
+  static const bool grid_env = getenv("STK_FUSED_GRID") && atoi(getenv("STK_FUSED_GRID"));
+  ctx->fcluster = grid_env ? 0 : 1;
   if (!ctx->fbar) {
     int dev = 0, nsm = 0, per = 0;
     CK(cudaGetDevice(&dev));
@@ -1188,9 +1200,9 @@ stk_status fused_assemble(stk_ctx* ctx) {
   std::vector<int> m(nl);
   for (int q = 0; q < nl; ++q) {
     const int64_t V = owned_vertices(ctx->lev[fl + q]);
-    m[q] = V <= single ? 1 : std::max(1, std::min(ctx->fgrid, (int)((V + 255) / 256)));
+    m[q] = V <= single ? 1 : std::max(1, std::min(ctx->fcluster ? FCL : ctx->fgrid, (int)((V + 255) / 256)));
   }
-  const int mc = m[nl - 1] == 1 ? 1 : std::max(1, std::min(ctx->fgrid, (ctx->cN + 7) / 8));
+  const int mc = m[nl - 1] == 1 ? 1 : std::max(1, std::min(ctx->fcluster ? FCL : ctx->fgrid, (ctx->cN + 7) / 8));
   std::vector<FPhase> prog;
   auto add = [&](int op, int lev, int mm, int color = 0, int flip = 0) {
     FPhase P{};
