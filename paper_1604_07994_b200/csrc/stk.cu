@@ -125,7 +125,7 @@ struct stk_ctx {
   std::vector<int64_t> graph_sig;         // what the captured coarse graph depends on
   FPhase* fprog = nullptr;                // phase program of the fused V-cycle (device)
   int fnph = 0, fgrid_used = 0;
-  int fcluster = 1;  // fused V-cycle on one 16-CTA thread-block cluster (cluster barriers) when it fits
+  int fcluster = 0;  // fused V-cycle on one 16-CTA thread-block cluster (cluster barriers)
   double* cfac = nullptr;                 // Gauss-Jordan column factors
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // reductions
@@ -1127,8 +1127,13 @@ stk_status op_gmres(stk_ctx* ctx, const double* b, double* x, double rtol, int m
 
 // persistent-grid size (one 256-thread CTA per SM) and the barrier words
 stk_status fused_setup(stk_ctx* ctx) {
-  static const bool grid_env = getenv("STK_FUSED_GRID") && atoi(getenv("STK_FUSED_GRID"));
-  ctx->fcluster = grid_env ? 0 : 1;
+  // the fused V-cycle (off by default, stk_set_fuse_n) on one 16-CTA cluster with hardware
+  // cluster barriers (STK_FUSED_CLUSTER=1) or on a cooperative grid with the software grid
+  // barrier over the participating CTA prefix (default: faster for the one-CTA phases of
+  // the n <= 8 levels; cfg3 n = 256, fuse_n = 8: 16.3 vs 16.7 ms per cycle; both slower than
+  // the graph of per-phase launches, 15.96 ms, profiles/r02_levels_fused_cluster.log)
+  static const bool cl_env = getenv("STK_FUSED_CLUSTER") && atoi(getenv("STK_FUSED_CLUSTER"));
+  ctx->fcluster = cl_env ? 1 : 0;
   if (!ctx->fbar) {
     int dev = 0, nsm = 0, per = 0;
     CK(cudaGetDevice(&dev));
