@@ -173,6 +173,17 @@ stk_status stk_import(stk_ctx* ctx, int32_t level, const double* canon, int32_t 
                       double* dev_vec);
 stk_status stk_export(stk_ctx* ctx, int32_t level, const double* dev_vec, double* canon,
                       int32_t where);
+/* The stabilised P1-P0 operator (§3.3-3.4) on the finest
+ * level: P1 velocity as above, one pressure per tetrahedron,
+ *   y  = A u + B0^T p0          (velocity fields of the device level vectors x, y)
+ *   y0 = B0 u - C0 p0           (device arrays of 6 n^3 doubles, element order of the
+ *                                classes: e = 6 (i + n (j + n k)) + t)
+ * with b(v,q) = -(div v, q) and the facet-jump stabilisation of eq. (stabc)
+ * (P:550-557): c(p,q) = gamma sum_i 1/(2 mu_i) sum_{F interior facet of Omega_i}
+ * |T1||T2|/(|T1|+|T2|) [p][q] -- no jump penalised across Gamma_12 or on the
+ * boundary; gamma = 1 in the paper's experiments.  The pressure field of x
+ * is not read.  nranks == 1 only (STK_EUNSUP otherwise); STK_EINVAL for gamma <= 0. */
+stk_status stk_p0_apply(stk_ctx* ctx, const double* x, const double* p0, double* y, double* y0, double gamma);
 /* Coarsest-level solver, taking effect at the next stk_assemble.  kind 0 (default): the
  * exact solve of the A_tr coarse system by a dense inverse ("a direct coarse grid
  * solver ... is not problematic").  kind 1: the paper's Krylov coarse solver:

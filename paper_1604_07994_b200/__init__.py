@@ -74,6 +74,7 @@ _sigs = {
     "stk_export": [_P, ctypes.c_int32, _P, _P, ctypes.c_int32],
     "stk_zero_eliminated": [_P, ctypes.c_int32, _P],
     "stk_set_coarse_solver": [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32],
+    "stk_p0_apply": [_P, _P, _P, _P, _P, ctypes.c_double],
     "stk_load_vector": [_P, ctypes.c_int32, _P, _P, ctypes.c_int32, _P],
     "stk_apply": [_P, ctypes.c_int32, ctypes.c_uint32, _P, _P],
     "stk_residual": [_P, ctypes.c_int32, _P, _P, _P, _P],
@@ -267,6 +268,15 @@ class StokesContext:
 
     def assemble(self):
         self._chk("stk_assemble", _lib.stk_assemble(self.h))
+
+    def p0_apply(self, x, p0, y=None, y0=None, gamma=1.0):
+        """Stabilised P1-P0 operator: y = A u + B0^T p0 (level-0
+        vector), y0 = B0 u - C0 p0 (6 n^3 per-tet pressures, device tensor)."""
+        y = self.new_vector(0) if y is None else y
+        p0 = p0.contiguous()
+        y0 = self.torch.empty_like(p0) if y0 is None else y0
+        self._chk("stk_p0_apply", _lib.stk_p0_apply(self.h, _ptr(x), _ptr(p0), _ptr(y), _ptr(y0), gamma))
+        return y, y0
 
     def set_coarse_solver(self, kind="direct", minres_its=20, cg_its=4):
         """Coarsest-level solver: "direct" (dense inverse of the A_tr system) or "minres"

@@ -18,6 +18,7 @@
 #include "kernels_sweep.cuh"
 #include "krylov.cuh"
 #include "kernels_minres.cuh"
+#include "kernels_p0.cuh"
 
 using namespace stk;
 
@@ -1744,6 +1745,23 @@ stk_status stk_import(stk_ctx* ctx, int32_t level, const double* canon, int32_t 
   if (staging) CK(cudaFreeAsync(staging, ctx->stream));
   if (where == STK_HOST) CK(cudaStreamSynchronize(ctx->stream));
   return s;
+}
+
+stk_status stk_p0_apply(stk_ctx* ctx, const double* x, const double* p0, double* y, double* y0, double gamma) {
+  ST(check(ctx, 2));
+  if (!x || !p0 || !y || !y0 || !(gamma > 0)) return STK_EINVAL;
+  if (ctx->cfg.nranks != 1) {
+    ctx->err = "stk_p0_apply: one rank only";
+    return STK_EUNSUP;
+  }
+  Level& L = ctx->lev[0];
+  const DGrid g = dgrid(ctx, L);
+  ST(op_apply(ctx, 0, BLK_A, x, y));  // A u (the velocity block is the P1-P1 scheme's)
+  k_p0_bt<<<nblocks(owned_vertices(L)), kThreads, 0, ctx->stream>>>(g, p0, y);
+  ST(launched(ctx));
+  const int64_t E = (int64_t)6 * L.n * L.n * L.n;
+  k_p0_rows<<<nblocks(E), kThreads, 0, ctx->stream>>>(g, x, p0, y0, gamma);
+  return launched(ctx);
 }
 
 stk_status stk_set_coarse_solver(stk_ctx* ctx, int32_t kind, int32_t minres_its, int32_t cg_its) {
