@@ -184,6 +184,12 @@ stk_status stk_export(stk_ctx* ctx, int32_t level, const double* dev_vec, double
  * boundary; gamma = 1 in the paper's experiments.  The pressure field of x
  * is not read.  nranks == 1 only (STK_EUNSUP otherwise); STK_EINVAL for gamma <= 0. */
 stk_status stk_p0_apply(stk_ctx* ctx, const double* x, const double* p0, double* y, double* y0, double gamma);
+/* The local flux post-process of the P1-P0 scheme: flux[4 e + m] (device,
+ * 4 x 6 n^3 doubles) = int_F j_{F;T} over the facet of tet e opposite its local Kuhn
+ * vertex m: int_F u_h . n_T plus, on facets interior to one isoviscous subdomain,
+ * gamma/(2 mu) |T||T'|/(|T|+|T'|) (p_T - p_T').  For a discrete solution with zero
+ * mass rhs every element's four fluxes sum to 0 (exact element-wise conservation). */
+stk_status stk_p0_fluxes(stk_ctx* ctx, const double* x, const double* p0, double* flux, double gamma);
 /* Coarsest-level solver, taking effect at the next stk_assemble.  kind 0 (default): the
  * exact solve of the A_tr coarse system by a dense inverse ("a direct coarse grid
  * solver ... is not problematic").  kind 1: the paper's Krylov coarse solver:

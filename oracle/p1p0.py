@@ -130,6 +130,39 @@ class P0Problem:
             x[3 * self.V:] = p - (self.vol @ p) / self.vol.sum()
         return x
 
+    def facet_fluxes(self, x):
+        """per element T and local vertex m, int_F j_{F;T} over the facet F
+        opposite m: int_F u_h . n_T (exact for P1: |F| times the mean of u over the facet's
+        3 vertices, n_T outward) plus, on facets interior to one subdomain, int_F Delta j
+        = gamma/(2 mu) |T||T^F|/(|T|+|T^F|) (p_T - p_{T^F}).  Returns (E, 4)."""
+        V = self.V
+        u = x[:3 * V].reshape(3, V)
+        p = x[3 * V:]
+        out = np.zeros((self.E, 4))
+        for m in range(4):
+            g = self.grads[:, m]
+            gn = np.linalg.norm(g, axis=1)
+            area = 3.0 * self.vol * gn
+            nrm = -g / gn[:, None]
+            ubar = np.zeros((self.E, 3))
+            for q in range(4):
+                if q != m:
+                    ubar += u[:, self.vid[:, q]].T / 3.0
+            out[:, m] = area * np.sum(ubar * nrm, axis=1)
+        # Delta j across interior same-viscosity facets: find the local index of the
+        # facet in each tet (the vertex of the tet not on the facet)
+        T1, T2, area, normal = facets(self.n)
+        same = self.mu[T1] == self.mu[T2]
+        for A, Bt in ((T1, T2), (T2, T1)):
+            shared = np.zeros(len(A), dtype=np.int64)
+            for m in range(4):
+                v = self.vid[A, m]
+                onB = (self.vid[Bt] == v[:, None]).any(axis=1)
+                shared = np.where(~onB, m, shared)
+            w = self.gamma / (2.0 * self.mu[A]) * self.vol[A] * self.vol[Bt] / (self.vol[A] + self.vol[Bt])
+            np.add.at(out, (A[same], shared[same]), (w * (p[A] - p[Bt]))[same])
+        return out
+
     def facet_flux_balance(self, x):
         """per element, sum over its interior facets of int_F j_{F;T} plus the
         velocity flux through its boundary facets (div theorem: |T| div u_T); returns

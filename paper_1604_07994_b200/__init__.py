@@ -75,6 +75,7 @@ _sigs = {
     "stk_zero_eliminated": [_P, ctypes.c_int32, _P],
     "stk_set_coarse_solver": [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32],
     "stk_p0_apply": [_P, _P, _P, _P, _P, ctypes.c_double],
+    "stk_p0_fluxes": [_P, _P, _P, _P, ctypes.c_double],
     "stk_load_vector": [_P, ctypes.c_int32, _P, _P, ctypes.c_int32, _P],
     "stk_apply": [_P, ctypes.c_int32, ctypes.c_uint32, _P, _P],
     "stk_residual": [_P, ctypes.c_int32, _P, _P, _P, _P],
@@ -277,6 +278,13 @@ class StokesContext:
         y0 = self.torch.empty_like(p0) if y0 is None else y0
         self._chk("stk_p0_apply", _lib.stk_p0_apply(self.h, _ptr(x), _ptr(p0), _ptr(y), _ptr(y0), gamma))
         return y, y0
+
+    def p0_fluxes(self, x, p0, gamma=1.0):
+        """P1-P0 local flux post-process: (6 n^3, 4) facet fluxes."""
+        p0 = p0.contiguous()
+        fl = self.torch.empty((p0.numel(), 4), dtype=self.torch.float64, device=p0.device)
+        self._chk("stk_p0_fluxes", _lib.stk_p0_fluxes(self.h, _ptr(x), _ptr(p0), _ptr(fl), gamma))
+        return fl
 
     def set_coarse_solver(self, kind="direct", minres_its=20, cg_its=4):
         """Coarsest-level solver: "direct" (dense inverse of the A_tr system) or "minres"

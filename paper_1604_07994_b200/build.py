@@ -47,6 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 "-Xlinker", "-rpath=" + os.path.join(nd, "lib")]
     else:
         cmd += ["-DSTK_HAVE_NCCL=0"]
+    extra = os.environ.get("STK_EXTRA_FLAGS", "").split()   # experiments: -D switches
+    cmd += extra
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -156,4 +156,46 @@ __global__ void k_p0_rows(DGrid g, const double* __restrict__ u, const double* _
   y0[e] = -vol * div - cp;
 }
 
+// local flux post-process: flux[4 e + m] = int_F j_{F;T} over the facet of
+// tet e opposite its local vertex m: int_F u_h . n_T = -|T| grad lambda_m . sum_{q != m} u_q
+// (|F| = 3 |T| |grad lambda_m|, n_T = -grad lambda_m / |grad lambda_m|, the facet mean of
+// a P1 field is the mean of its 3 vertices), plus w_F (p_T - p_T') on facets interior to
+// one subdomain.  sum_m flux[4 e + m] = |T| div u_T + sum_F w_F (p_T - p_T') = -(B0 u -
+// C0 p)_T: zero at a discrete solution with zero mass rhs (element-wise conservation).
+__global__ void k_p0_fluxes(DGrid g, const double* __restrict__ u, const double* __restrict__ p0,
+                            double* __restrict__ flux, double gamma) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int n = g.n;
+  if (e >= (int64_t)6 * n * n * n) return;
+  const int t = (int)(e % 6);
+  int64_t r = e / 6;
+  const int ci = (int)(r % n);
+  r /= n;
+  const int cj = (int)(r % n), ck = (int)(r / n);
+  const double hinv = 1.0 / g.h, vol = g.h * g.h * g.h / 6.0;
+  double uq[4][3];
+  for (int q = 0; q < 4; ++q) {
+    const int c = ktet_corner(t, q);
+    const int64_t o = vidx(g, ci + (c & 1), cj + ((c >> 1) & 1), ck + (c >> 2));
+    for (int a = 0; a < 3; ++a) uq[q][a] = u[a * g.fs + o];
+  }
+  const double mu = mu_of(g, elem_class(g, ci, cj, ck, t));
+  const double w = gamma / (2.0 * mu) * (0.5 * vol);
+  const double pt = p0[e];
+  for (int m = 0; m < 4; ++m) {
+    double gm[3];
+    p0_grad(t, m, hinv, gm);
+    double s = 0.0;
+    for (int q = 0; q < 4; ++q)
+      if (q != m) s += gm[0] * uq[q][0] + gm[1] * uq[q][1] + gm[2] * uq[q][2];
+    double f = -vol * s;
+    const int ni = ci + c_fnb.dx[t][m], nj = cj + c_fnb.dy[t][m], nk = ck + c_fnb.dz[t][m];
+    if (ni >= 0 && nj >= 0 && nk >= 0 && ni < n && nj < n && nk < n) {
+      const int tn = c_fnb.tn[t][m];
+      if (mu_of(g, elem_class(g, ni, nj, nk, tn)) == mu) f += w * (pt - p0[((((int64_t)nk * n) + nj) * n + ni) * 6 + tn]);
+    }
+    flux[4 * e + m] = f;
+  }
+}
+
 }  // namespace stk

@@ -969,7 +969,10 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
       release();
       o += g.py;
     };
-    if constexpr (OP != OP_VEL) {
+#ifndef STK_UNROLL3_MASK
+#define STK_UNROLL3_MASK (1 << OP_VEL)
+#endif
+    if constexpr (!((STK_UNROLL3_MASK >> OP) & 1)) {
       // one body instance, the accumulators rotate by register moves: 3x less code
       // (measured faster for these OPs; the velocity pass keeps the 3-way unroll)
 #pragma unroll 1

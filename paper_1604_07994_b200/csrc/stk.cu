@@ -1764,6 +1764,19 @@ stk_status stk_p0_apply(stk_ctx* ctx, const double* x, const double* p0, double*
   return launched(ctx);
 }
 
+stk_status stk_p0_fluxes(stk_ctx* ctx, const double* x, const double* p0, double* flux, double gamma) {
+  ST(check(ctx, 2));
+  if (!x || !p0 || !flux || !(gamma > 0)) return STK_EINVAL;
+  if (ctx->cfg.nranks != 1) {
+    ctx->err = "stk_p0_fluxes: one rank only";
+    return STK_EUNSUP;
+  }
+  Level& L = ctx->lev[0];
+  const int64_t E = (int64_t)6 * L.n * L.n * L.n;
+  k_p0_fluxes<<<nblocks(E), kThreads, 0, ctx->stream>>>(dgrid(ctx, L), x, p0, flux, gamma);
+  return launched(ctx);
+}
+
 stk_status stk_set_coarse_solver(stk_ctx* ctx, int32_t kind, int32_t minres_its, int32_t cg_its) {
   if (!ctx || kind < 0 || kind > 1 || minres_its < 1 || minres_its > 10000 || cg_its < 0 || cg_its > 10000)
     return STK_EINVAL;

@@ -127,3 +127,28 @@ def test_couette_flow_against_the_paper_table():
     rV = np.log2(res[0][1] / res[1][1])
     assert 1.85 < rL2 < 2.1 and 0.95 < rV < 1.15, (rL2, rV)
     assert np.log2(res[0][2] / res[1][2]) > 1.0
+
+
+def test_facet_fluxes_sum_to_the_element_balance_and_are_antisymmetric():
+    """the per-facet post-processed fluxes of an element sum to its balance
+    (|T| div u_T + sum_F int Delta j), and across an interior facet the two elements'
+    fluxes are opposite (u_h . n and the jump term change sign together)."""
+    n = 3
+    cfg = synth.get_config("cfg1", n=n)
+    cls, _ = synth.element_classes(cfg)
+    mu = np.asarray(cfg.class_mu)[cls]
+    pr = p1p0.P0Problem(n, mu, (synth.TRACTION,) * 5 + (synth.DIRICHLET,))
+    rng = np.random.default_rng(9)
+    x = np.where(pr.free, rng.standard_normal(3 * pr.V + pr.E), 0.0)
+    fl = pr.facet_fluxes(x)
+    np.testing.assert_allclose(fl.sum(axis=1), pr.facet_flux_balance(x), atol=1e-14)
+    T1, T2, _, _ = p1p0.facets(n)
+
+    def local(A, B):     # local index (opposite vertex) of the shared facet in tet A
+        return np.array([[m for m in range(4) if pr.vid[a, m] not in pr.vid[b]][0] for a, b in zip(A, B)])
+
+    f1 = fl[T1, local(T1, T2)]
+    f2 = fl[T2, local(T2, T1)]
+    np.testing.assert_allclose(f1, -f2, atol=1e-14)
+    same = mu[T1] == mu[T2]
+    assert same.any() and (~same).any()
