@@ -190,6 +190,18 @@ stk_status stk_p0_apply(stk_ctx* ctx, const double* x, const double* p0, double*
  * gamma/(2 mu) |T||T'|/(|T|+|T'|) (p_T - p_T').  For a discrete solution with zero
  * mass rhs every element's four fluxes sum to 0 (exact element-wise conservation). */
 stk_status stk_p0_fluxes(stk_ctx* ctx, const double* x, const double* p0, double* flux, double gamma);
+/* Solve the P1-P0 system K0 (u, p0) = (b_u, b0) from the given (x_u, x0) (device; b_u,
+ * x_u level-0 vectors whose pressure field is ignored, b_u 0 at eliminated DoFs; b0, x0
+ * 6 n^3 per-tet values) to ||b - K0 x|| / ||b|| <= rtol: right-preconditioned GMRES(m)
+ * (1 <= m <= 31, CGS2) whose preconditioner maps the P0 residual to the P1 pressure
+ * (each tet's integral shared by its 4 vertices), applies one V_var cycle of the P1-P1
+ * multigrid of this context (same velocity space and form) and averages the P1
+ * pressure correction per tet.  Without traction faces the mean of p0 is removed at
+ * the end.  Synchronous; report gets iterations, residual history and device time.
+ * nranks == 1 only; STK_ENOCONV (positive, x holds the last iterate) if rtol is not
+ * reached within max_its preconditioner applications. */
+stk_status stk_p0_solve(stk_ctx* ctx, const double* b_u, const double* b0, double* x_u, double* x0, double gamma,
+                        double rtol, int32_t max_its, int32_t m, stk_report* report);
 /* Coarsest-level solver, taking effect at the next stk_assemble.  kind 0 (default): the
  * exact solve of the A_tr coarse system by a dense inverse ("a direct coarse grid
  * solver ... is not problematic").  kind 1: the paper's Krylov coarse solver:

@@ -76,6 +76,7 @@ _sigs = {
     "stk_set_coarse_solver": [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32],
     "stk_p0_apply": [_P, _P, _P, _P, _P, ctypes.c_double],
     "stk_p0_fluxes": [_P, _P, _P, _P, ctypes.c_double],
+    "stk_p0_solve": [_P, _P, _P, _P, _P, ctypes.c_double, ctypes.c_double, ctypes.c_int32, ctypes.c_int32, _P],
     "stk_load_vector": [_P, ctypes.c_int32, _P, _P, ctypes.c_int32, _P],
     "stk_apply": [_P, ctypes.c_int32, ctypes.c_uint32, _P, _P],
     "stk_residual": [_P, ctypes.c_int32, _P, _P, _P, _P],
@@ -278,6 +279,17 @@ class StokesContext:
         y0 = self.torch.empty_like(p0) if y0 is None else y0
         self._chk("stk_p0_apply", _lib.stk_p0_apply(self.h, _ptr(x), _ptr(p0), _ptr(y), _ptr(y0), gamma))
         return y, y0
+
+    def p0_solve(self, b, b0, x=None, x0=None, gamma=1.0, rtol=1e-8, max_its=300, m=30):
+        """P1-P0 solve (stk_p0_solve): returns (x level vector, x0 per-tet tensor, report)."""
+        x = self.new_vector(0) if x is None else x
+        b0 = b0.contiguous()
+        x0 = self.torch.zeros_like(b0) if x0 is None else x0
+        rep = stk_report()
+        s = _lib.stk_p0_solve(self.h, _ptr(b), _ptr(b0), _ptr(x), _ptr(x0), gamma, rtol, max_its, m,
+                              ctypes.byref(rep))
+        self._chk("stk_p0_solve", s, allow=(STK_OK, STK_ENOCONV))
+        return x, x0, rep
 
     def p0_fluxes(self, x, p0, gamma=1.0):
         """P1-P0 local flux post-process: (6 n^3, 4) facet fluxes."""

@@ -156,6 +156,39 @@ __global__ void k_p0_rows(DGrid g, const double* __restrict__ u, const double* _
   y0[e] = -vol * div - cp;
 }
 
+// auxiliary-space maps between the P0 and the P1 pressure (stk_p0_solve's
+// preconditioner): a P0 residual (per-tet integrals) is shared equally by the tet's 4
+// vertices -- the transpose of the tet average -- and a P1 correction is averaged over
+// each tet's 4 vertices
+__global__ void k_p0_to_p1(DGrid g, const double* __restrict__ r0, double* __restrict__ bp) {
+  int i, j, k;
+  if (!owned_vertex(g, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, i, j, k)) return;
+  double acc = 0.0;
+  for (int own = 0; own < 8; ++own) {
+    const int ci = i - (own & 1), cj = j - ((own >> 1) & 1), ck = k - (own >> 2);
+    if (ci < 0 || cj < 0 || ck < 0 || ci >= g.n || cj >= g.n || ck >= g.n) continue;
+    for (int t = 0; t < 6; ++t)
+      if (kcorner(own, t) >= 0) acc += 0.25 * r0[((((int64_t)ck * g.n) + cj) * g.n + ci) * 6 + t];
+  }
+  bp[vidx(g, i, j, k)] = acc;
+}
+__global__ void k_p1_to_p0(DGrid g, const double* __restrict__ zp, double* __restrict__ z0) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int n = g.n;
+  if (e >= (int64_t)6 * n * n * n) return;
+  const int t = (int)(e % 6);
+  int64_t r = e / 6;
+  const int ci = (int)(r % n);
+  r /= n;
+  const int cj = (int)(r % n), ck = (int)(r / n);
+  double s = 0.0;
+  for (int q = 0; q < 4; ++q) {
+    const int c = ktet_corner(t, q);
+    s += zp[vidx(g, ci + (c & 1), cj + ((c >> 1) & 1), ck + (c >> 2))];
+  }
+  z0[e] = 0.25 * s;
+}
+
 // local flux post-process: flux[4 e + m] = int_F j_{F;T} over the facet of
 // tet e opposite its local vertex m: int_F u_h . n_T = -|T| grad lambda_m . sum_{q != m} u_q
 // (|F| = 3 |T| |grad lambda_m|, n_T = -grad lambda_m / |grad lambda_m|, the facet mean of

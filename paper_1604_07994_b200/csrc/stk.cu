@@ -148,6 +148,9 @@ struct stk_ctx {
   // coarsest-level solver: 0 dense inverse of the A_tr system (default), 1 the paper's
   // MINRES on A_sym with the corrected right-hand side (kernels_minres.cuh)
   int coarse_kind = 0, mr_its = 20, mr_cg = 4;
+  // P1-P0 solver workspace (stk_p0_solve): composite vectors [level-0 vector | 6 n^3]
+  double* p0ws = nullptr;
+  size_t cap_p0ws = 0;
   double* mr_S = nullptr;     // A_sym explicit stencils of every coarsest-level vertex
   int32_t* mr_rows = nullptr;
   double* mr_work = nullptr;
@@ -1777,6 +1780,198 @@ stk_status stk_p0_fluxes(stk_ctx* ctx, const double* x, const double* p0, double
   return launched(ctx);
 }
 
+__global__ void k_fill(double* __restrict__ a, int64_t n, double v) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    a[e] = v;
+}
+
+// The P1-P0 system K0 (u, p0) = (b_u, b0) by right-preconditioned GMRES(m) (CGS2, as
+// op_gmres) over composite vectors [level-0 vector (pressure field kept 0) | 6 n^3 per-tet
+// pressures].  Preconditioner (auxiliary space): the P0 residual is shared by the 4
+// vertices of each tet (k_p0_to_p1), one V_var cycle of the library's P1-P1 multigrid
+// (same velocity space and viscous form) is applied, and the P1 pressure correction is
+// averaged per tet (k_p1_to_p0).
+stk_status stk_p0_solve(stk_ctx* ctx, const double* bu, const double* b0, double* xu, double* x0, double gamma,
+                        double rtol, int32_t max_its, int32_t m, stk_report* rep) {
+  ST(check(ctx, 2));
+  if (!bu || !b0 || !xu || !x0 || !(gamma > 0) || m < 1 || m + 1 > KRY_MAXV || max_its < 1) return STK_EINVAL;
+  if (ctx->cfg.nranks != 1) {
+    ctx->err = "stk_p0_solve: one rank only";
+    return STK_EUNSUP;
+  }
+  Level& L = ctx->lev[0];
+  const DGrid g = dgrid(ctx, L);
+  const int64_t vlen = L.vlen, fs = L.fs, E = (int64_t)6 * L.n * L.n * L.n, clen = vlen + E;
+  const size_t cb = sizeof(double) * clen;
+  // basis (m+1), Z (m), b, x, r, w, two level vectors, ones(E), partials
+  const size_t need = (size_t)clen * (2 * m + 5) + 2 * (size_t)vlen + E + (size_t)kGsBlocks * (KRY_MAXV + 1) + 128;
+  if (!ensure(ctx->p0ws, ctx->cap_p0ws, need)) return STK_ENOMEM;
+  CK(cudaMemsetAsync(ctx->p0ws, 0, sizeof(double) * need, ctx->stream));
+  double* Vb = ctx->p0ws;
+  double* Zb = Vb + (size_t)clen * (m + 1);
+  double* B = Zb + (size_t)clen * m;
+  double* X = B + clen;
+  double* R = X + clen;
+  double* W = R + clen;
+  double* pb = W + clen;
+  double* zl = pb + vlen;
+  double* ones = zl + vlen;
+  double* part = ones + E;
+  double* coef = part + (size_t)kGsBlocks * (KRY_MAXV + 1);  // 128 device scalars
+  auto V = [&](int q) { return Vb + (size_t)q * clen; };
+  auto Zq = [&](int q) { return Zb + (size_t)q * clen; };
+  k_fill<<<256, 256, 0, ctx->stream>>>(ones, E, 1.0);
+  ST(launched(ctx));
+  // composite b, x (level parts without the pressure field)
+  CK(cudaMemcpyAsync(B, bu, sizeof(double) * 3 * fs, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(B + vlen, b0, sizeof(double) * E, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(X, xu, sizeof(double) * 3 * fs, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(X + vlen, x0, sizeof(double) * E, cudaMemcpyDeviceToDevice, ctx->stream));
+  const unsigned nbv = nblocks(owned_vertices(L)), nbe = nblocks(E);
+  auto Kop = [&](const double* in, double* out) -> stk_status {
+    ST(op_apply(ctx, 0, BLK_A, in, out));
+    k_p0_bt<<<nbv, kThreads, 0, ctx->stream>>>(g, in + vlen, out);
+    ST(launched(ctx));
+    k_p0_rows<<<nbe, kThreads, 0, ctx->stream>>>(g, in, in + vlen, out + vlen, gamma);
+    return launched(ctx);
+  };
+  auto Minv = [&](const double* in, double* out) -> stk_status {
+    CK(cudaMemcpyAsync(pb, in, sizeof(double) * 3 * fs, cudaMemcpyDeviceToDevice, ctx->stream));
+    k_p0_to_p1<<<nbv, kThreads, 0, ctx->stream>>>(g, in + vlen, pb + 3 * fs);
+    ST(launched(ctx));
+    CK(cudaMemsetAsync(zl, 0, sizeof(double) * vlen, ctx->stream));
+    ST(op_vcycle(ctx, 0, pb, zl));
+    CK(cudaMemcpyAsync(out, zl, sizeof(double) * 3 * fs, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemsetAsync(out + 3 * fs, 0, sizeof(double) * fs, ctx->stream));
+    k_p1_to_p0<<<nbe, kThreads, 0, ctx->stream>>>(g, zl + 3 * fs, out + vlen);
+    return launched(ctx);
+  };
+  // flat CGS passes over composite vectors (k_gs_pass with the composite length)
+  auto gs = [&](int mode, const double* Vp, int nv, double* w, const double* c, double* out, int cnt) -> stk_status {
+    switch (mode) {
+      case GS_DOTS: k_gs_pass<GS_DOTS, KRY_MAXV><<<kGsBlocks, 256, 0, ctx->stream>>>(Vp, clen, nv, w, c, part); break;
+      case GS_UPDATE_DOTS:
+        k_gs_pass<GS_UPDATE_DOTS, KRY_MAXV><<<kGsBlocks, 256, 0, ctx->stream>>>(Vp, clen, nv, w, c, part);
+        break;
+      default: k_gs_pass<GS_UPDATE_NORM, KRY_MAXV><<<kGsBlocks, 256, 0, ctx->stream>>>(Vp, clen, nv, w, c, part);
+    }
+    ST(launched(ctx));
+    k_gs_final<<<1, 64, 0, ctx->stream>>>(part, kGsBlocks, cnt, out);
+    return launched(ctx);
+  };
+  auto host = [&](const double* d, int cnt, double* h) -> stk_status {
+    CK(cudaMemcpyAsync(h, d, sizeof(double) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return STK_OK;
+  };
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, ctx->stream));
+  stk_report local{};
+  stk_report* Rp = rep ? rep : &local;
+  memset(Rp, 0, sizeof(*Rp));
+  double nb2 = 0.0, nr2 = 0.0;
+  ST(gs(GS_DOTS, B, 0, B, nullptr, coef, 1));  // ||b||^2 (slot nv = 0)
+  ST(host(coef, 1, &nb2));
+  const double bnorm = std::sqrt(nb2);
+  auto residual = [&]() -> stk_status {  // R = B - K X, returns ||R||^2 in nr2
+    ST(Kop(X, R));
+    k_axpby_flat<<<kGsBlocks, 256, 0, ctx->stream>>>(clen, 1.0, B, -1.0, R);
+    ST(launched(ctx));
+    ST(gs(GS_DOTS, R, 0, R, nullptr, coef, 1));
+    return host(coef, 1, &nr2);
+  };
+  ST(residual());
+  double beta = std::sqrt(nr2), rel = bnorm > 0 ? beta / bnorm : 0.0;
+  Rp->res_hist[0] = rel;
+  int its = 0;
+  std::vector<double> H((m + 1) * m, 0.0), cs(m), sn(m), gv(m + 1), h(m + 1), y(m), hc(3 * (m + 2));
+  while (rel > rtol && its < max_its) {
+    k_axpby_flat<<<kGsBlocks, 256, 0, ctx->stream>>>(clen, 1.0 / beta, R, 0.0, V(0));
+    ST(launched(ctx));
+    std::fill(gv.begin(), gv.end(), 0.0);
+    gv[0] = beta;
+    int jdone = 0;
+    for (int j = 0; j < m && its < max_its; ++j) {
+      ST(Minv(V(j), Zq(j)));
+      ST(Kop(Zq(j), W));
+      double* c1 = coef;
+      double* c2 = coef + (m + 2);
+      double* nw = coef + 2 * (m + 2);
+      ST(gs(GS_DOTS, V(0), j + 1, W, nullptr, c1, j + 1));
+      ST(gs(GS_UPDATE_DOTS, V(0), j + 1, W, c1, c2, j + 1));
+      ST(gs(GS_UPDATE_NORM, V(0), j + 1, W, c2, nw, 1));
+      ST(host(coef, 3 * (m + 2), hc.data()));
+      for (int q = 0; q <= j; ++q) h[q] = hc[q] + hc[(m + 2) + q];
+      h[j + 1] = std::sqrt(std::max(hc[2 * (m + 2)], 0.0));
+      if (h[j + 1] > 0) {
+        k_axpby_flat<<<kGsBlocks, 256, 0, ctx->stream>>>(clen, 1.0 / h[j + 1], W, 0.0, V(j + 1));
+        ST(launched(ctx));
+      }
+      for (int q = 0; q < j; ++q) {
+        const double t = cs[q] * h[q] + sn[q] * h[q + 1];
+        h[q + 1] = -sn[q] * h[q] + cs[q] * h[q + 1];
+        h[q] = t;
+      }
+      const double den = std::hypot(h[j], h[j + 1]);
+      cs[j] = den > 0 ? h[j] / den : 1.0;
+      sn[j] = den > 0 ? h[j + 1] / den : 0.0;
+      h[j] = den;
+      h[j + 1] = 0.0;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      for (int q = 0; q <= j; ++q) H[q * m + j] = h[q];
+      ++its;
+      jdone = j + 1;
+      rel = bnorm > 0 ? std::fabs(gv[j + 1]) / bnorm : 0.0;
+      if (its < 256) Rp->res_hist[its] = rel;
+      if (!std::isfinite(rel)) {
+        Rp->nan_seen = 1;
+        break;
+      }
+      if (rel <= rtol) break;
+    }
+    for (int q = jdone - 1; q >= 0; --q) {
+      double s = gv[q];
+      for (int c = q + 1; c < jdone; ++c) s -= H[q * m + c] * y[c];
+      y[q] = s / H[q * m + q];
+    }
+    for (int q = 0; q < jdone; ++q) {
+      k_axpby_flat<<<kGsBlocks, 256, 0, ctx->stream>>>(clen, y[q], Zq(q), 1.0, X);
+      ST(launched(ctx));
+    }
+    ST(residual());
+    beta = std::sqrt(nr2);
+    rel = bnorm > 0 ? beta / bnorm : 0.0;
+    if (its < 256) Rp->res_hist[its] = rel;
+    if (Rp->nan_seen) break;
+  }
+  // the volume-weighted (all tets equal) mean of p0 removed when no face is traction free
+  if (!has_traction(ctx->cfg)) {
+    k_gs_pass<GS_DOTS, 8><<<kGsBlocks, 256, 0, ctx->stream>>>(ones, E, 1, X + vlen, nullptr, part);
+    ST(launched(ctx));
+    k_gs_final<<<1, 64, 0, ctx->stream>>>(part, kGsBlocks, 1, coef);
+    ST(launched(ctx));
+    double sp = 0.0;
+    ST(host(coef, 1, &sp));
+    k_axpby_flat<<<kGsBlocks, 256, 0, ctx->stream>>>(E, -sp / (double)E, ones, 1.0, X + vlen);
+    ST(launched(ctx));
+  }
+  CK(cudaMemcpyAsync(xu, X, sizeof(double) * 3 * fs, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(x0, X + vlen, sizeof(double) * E, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaEventRecord(e1, ctx->stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  Rp->cycles = its;
+  Rp->rel_res = rel;
+  Rp->t_total_s = ms * 1e-3;
+  return rel <= rtol ? STK_OK : STK_ENOCONV;
+}
+
 stk_status stk_set_coarse_solver(stk_ctx* ctx, int32_t kind, int32_t minres_its, int32_t cg_its) {
   if (!ctx || kind < 0 || kind > 1 || minres_its < 1 || minres_its > 10000 || cg_its < 0 || cg_its > 10000)
     return STK_EINVAL;
@@ -2149,6 +2344,7 @@ stk_status stk_destroy(stk_ctx* ctx) {
   cudaFree(ctx->kbasis);
   cudaFree(ctx->kwork);
   cudaFree(ctx->kz);
+  cudaFree(ctx->p0ws);
   cudaFree(ctx->kcoef);
   cudaFree(ctx->kpart);
   delete ctx;
