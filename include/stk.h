@@ -195,8 +195,9 @@ stk_status stk_p0_fluxes(stk_ctx* ctx, const double* x, const double* p0, double
  * 6 n^3 per-tet values) to ||b - K0 x|| / ||b|| <= rtol: right-preconditioned GMRES(m)
  * (1 <= m <= 31, CGS2) whose preconditioner maps the P0 residual to the P1 pressure
  * (each tet's integral shared by its 4 vertices), applies one V_var cycle of the P1-P1
- * multigrid of this context (same velocity space and form) and averages the P1
- * pressure correction per tet.  Without traction faces the mean of p0 is removed at
+ * multigrid of this context (same velocity space and form), averages the P1
+ * pressure correction per tet and adds the element-local term -(mu_T / 2|T|) r0 (the
+ * 1/mu-weighted P0 mass inverse, for the per-tet modes outside the P1 space).  Without traction faces the mean of p0 is removed at
  * the end.  Synchronous; report gets iterations, residual history and device time.
  * nranks == 1 only; STK_ENOCONV (positive, x holds the last iterate) if rtol is not
  * reached within max_its preconditioner applications. */

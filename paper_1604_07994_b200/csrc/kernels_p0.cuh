@@ -172,7 +172,12 @@ __global__ void k_p0_to_p1(DGrid g, const double* __restrict__ r0, double* __res
   }
   bp[vidx(g, i, j, k)] = acc;
 }
-__global__ void k_p1_to_p0(DGrid g, const double* __restrict__ zp, double* __restrict__ z0) {
+// (r0 != nullptr: plus the element-local Schur-complement term -wp (mu_T / |T|) r0, the
+// 1/mu-weighted P0 mass inverse -- it reaches the per-tet pressure modes the P1 auxiliary
+// space cannot represent; without it the preconditioner is singular on them and GMRES
+// stagnates near 1e-3)
+__global__ void k_p1_to_p0(DGrid g, const double* __restrict__ zp, double* __restrict__ z0,
+                           const double* __restrict__ r0 = nullptr, double wp = 0.0) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int n = g.n;
   if (e >= (int64_t)6 * n * n * n) return;
@@ -186,7 +191,9 @@ __global__ void k_p1_to_p0(DGrid g, const double* __restrict__ zp, double* __res
     const int c = ktet_corner(t, q);
     s += zp[vidx(g, ci + (c & 1), cj + ((c >> 1) & 1), ck + (c >> 2))];
   }
-  z0[e] = 0.25 * s;
+  double z = 0.25 * s;
+  if (r0) z -= wp * mu_of(g, elem_class(g, ci, cj, ck, t)) * (6.0 / (g.h * g.h * g.h)) * r0[e];
+  z0[e] = z;
 }
 
 // local flux post-process: flux[4 e + m] = int_F j_{F;T} over the facet of

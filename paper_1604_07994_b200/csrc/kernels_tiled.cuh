@@ -48,7 +48,19 @@ constexpr int TX = 32, TY = 8, NT = TX * TY;
 constexpr int HX = TX + 2, HY = TY + 2, PLANE = HX * HY;
 // shared-memory stride of one staged field plane: 128-byte aligned TMA destinations
 constexpr int FST = ((PLANE + 15) / 16) * 16;
-constexpr int PREF = 3, RING = PREF + 2;
+#ifndef STK_PREF
+#define STK_PREF 3
+#endif
+// STK_DECOUPLE=1: no per-plane __syncthreads.  Every warp releases plane S-2 on a
+// per-slot "empty" mbarrier (one arrival per warp) and runs on; the warp S % NW waits
+// for that barrier and stages plane S+RING-2 (the producer role rotates over the warps),
+// so the warps of a CTA drift up to PREF planes apart and their shared-memory, fp64 and
+// store phases overlap instead of running in lockstep.
+#ifndef STK_DECOUPLE
+#define STK_DECOUPLE 0
+#endif
+constexpr int PREF = STK_PREF, RING = PREF + 2;
+constexpr int NBAR = STK_DECOUPLE ? 2 * RING : RING;
 // per-row auxiliary fields, prefetched one row ahead by cp.async into a per-thread
 // double buffer: RESID b (4), VEL f (3), P1 g (1), P2 own p (1)
 __host__ __device__ constexpr int n_aux(int op) { return op == 1 ? 4 : op == 2 ? 3 : (op == 3 || op == 4) ? 1 : 0; }
@@ -209,6 +221,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -796,7 +811,7 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
       smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);  // 1 KB aligned TMA destinations
   double* ring = reinterpret_cast<double*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + RING * SLOT * sizeof(double));
-  double* auxb = reinterpret_cast<double*>(bars + RING);  // [2][NA][NT] per-thread aux double buffer
+  double* auxb = reinterpret_cast<double*>(bars + NBAR);  // [2][NA][NT] per-thread aux double buffer
 
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int ntx = g.n / TX;
@@ -815,6 +830,9 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RING; ++s) mbar_init(&bars[s], 1);
+#if STK_DECOUPLE
+    for (int s = 0; s < RING; ++s) mbar_init(&bars[RING + s], NT / 32);  // "empty": one arrival per warp
+#endif
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #if STK_TMA_PREFETCH
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapU) : "memory");
@@ -822,29 +840,38 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
 #endif
   }
   __syncthreads();
-  // Producer (thread 0): the planes of this CTA's items, items blockIdx.x + q G,
-  // back to back; global plane sequence number S selects slot S % RING.
-  int pq = 0, pp = 0, pS = 0, pi0 = 0, pj0 = 0, pkb = 0, pM = 0;
+  // Producer: the planes of this CTA's items, items blockIdx.x + q G, back to back;
+  // global plane sequence number S selects slot S % RING.  The sequence state is kept
+  // by thread 0 (or, STK_DECOUPLE, by every thread: the issuing warp rotates).
+  int pq = 0, pp = 0, pS = 0, pM = 0;   // item counter, plane within the item, sequence number, planes of the item
   bool pvalid = false;
-  if (threadIdx.x == 0 && (int)blockIdx.x < nitems) {
-    item_geom(blockIdx.x, pi0, pj0, pkb, pM);
+  auto item_planes = [&](int it) {
+    const int tkb = g.z0 + (it / tiles) * a.kchunk;
+    return min(tkb + a.kchunk, g.z0 + g.nzl) - tkb + 2;
+  };
+  if ((STK_DECOUPLE || threadIdx.x == 0) && (int)blockIdx.x < nitems) {
+    pM = item_planes(blockIdx.x);
     pvalid = true;
   }
-  auto issue_next = [&]() {  // thread 0: stage the next plane of the sequence
+  auto issue_next = [&](bool do_issue) {  // stage the next plane of the sequence (do_issue: this thread issues)
     if (!pvalid) return;
-    const int s = pS % RING;
-    const int P = pkb - 1 + pp;
+    if (do_issue) {
+      int pi0, pj0, pkb, pMM;
+      item_geom(blockIdx.x + pq * G, pi0, pj0, pkb, pMM);
+      const int s = pS % RING;
+      const int P = pkb - 1 + pp;
 #if STK_TMA_FENCE
-    fence_proxy_async();
+      fence_proxy_async();
 #endif
-    mbar_expect_tx(&bars[s], TX_BYTES);
-    double* dst = ring + s * SLOT;
-    if (NF == 4) {
-      for (int f = 0; f < 3; ++f)
-        tma_load_4d(dst + f * FST, &mapU, &bars[s], pi0 - 1 - a.ux0, pj0 - 1 - a.uy0, P - a.uz0, f);
-      tma_load_4d(dst + 3 * FST, &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
-    } else {
-      tma_load_4d(dst, &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
+      mbar_expect_tx(&bars[s], TX_BYTES);
+      double* dst = ring + s * SLOT;
+      if (NF == 4) {
+        for (int f = 0; f < 3; ++f)
+          tma_load_4d(dst + f * FST, &mapU, &bars[s], pi0 - 1 - a.ux0, pj0 - 1 - a.uy0, P - a.uz0, f);
+        tma_load_4d(dst + 3 * FST, &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
+      } else {
+        tma_load_4d(dst, &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
+      }
     }
     ++pS;
     if (++pp == pM) {
@@ -852,16 +879,16 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
       ++pq;
       const int it = blockIdx.x + pq * G;
       pvalid = it < nitems;
-      if (pvalid) item_geom(it, pi0, pj0, pkb, pM);
+      if (pvalid) pM = item_planes(it);
     }
   };
-  if (threadIdx.x == 0)
-    for (int q = 0; q < RING - 2; ++q) issue_next();  // consumer iteration S stages plane S+RING-2
+  if (STK_DECOUPLE || threadIdx.x == 0)
+    for (int q = 0; q < RING - 2; ++q) issue_next(threadIdx.x == 0);  // consumer iteration S stages plane S+RING-2
 
   int S = 0;  // consumer: global plane sequence number
   // debug trace (a.trace != nullptr): cycles in the plane waits, the per-plane
   // barrier and the producer's issue, for thread 0 and for the last warp's lane 0
-  const bool trc = a.trace != nullptr && (threadIdx.x == 0 || threadIdx.x == NT - 32);
+  const bool trc = !STK_DECOUPLE && a.trace != nullptr && (threadIdx.x == 0 || threadIdx.x == NT - 32);
   unsigned long long tw = 0, ts = 0, ti = 0, t_start = trc ? clock64() : 0;
   auto wait_plane = [&]() -> const double* {
     const int s = S % RING;
@@ -871,15 +898,29 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
     return ring + s * SLOT;
   };
   auto release = [&]() {  // all reads of plane S-2 are done: stage a new plane into its slot
+#if STK_DECOUPLE
+    constexpr int NW = NT / 32;
+    __syncwarp();
+    if (S >= 2 && (threadIdx.x & 31) == 0) mbar_arrive(&bars[RING + (S - 2) % RING]);
+    if ((S % NW) == (int)(threadIdx.x >> 5) && pvalid) {
+      // this warp's turn: every warp has released plane S-2 (slot of plane S+RING-2)
+      if (S >= 2) mbar_wait(&bars[RING + (S - 2) % RING], ((S - 2) / RING) & 1);
+      issue_next((threadIdx.x & 31) == 0);
+    } else {
+      issue_next(false);
+    }
+    ++S;
+#else
     const unsigned long long c0 = trc ? clock64() : 0;
     __syncthreads();
     const unsigned long long c1 = trc ? clock64() : 0;
-    if (threadIdx.x == 0) issue_next();
+    if (threadIdx.x == 0) issue_next(true);
     if (trc) {
       ts += c1 - c0;
       ti += clock64() - c1;
     }
     ++S;
+#endif
   };
   const int i_ofs = tx, j_ofs = ty;
   const int base = (ty + 1) * HX + (tx + 1);
@@ -1076,7 +1117,7 @@ inline bool assemble_stencils(cudaStream_t st) {
 }
 
 inline size_t stream_smem(int op) {
-  return 1024 + RING * slot_doubles(op) * sizeof(double) + RING * sizeof(uint64_t) + 2 * n_aux(op) * NT * sizeof(double);
+  return 1024 + RING * slot_doubles(op) * sizeof(double) + NBAR * sizeof(uint64_t) + 2 * n_aux(op) * NT * sizeof(double);
 }
 
 // the irregular-row list of a level (built by stk_assemble)

@@ -1843,7 +1843,7 @@ stk_status stk_p0_solve(stk_ctx* ctx, const double* bu, const double* b0, double
     ST(op_vcycle(ctx, 0, pb, zl));
     CK(cudaMemcpyAsync(out, zl, sizeof(double) * 3 * fs, cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaMemsetAsync(out + 3 * fs, 0, sizeof(double) * fs, ctx->stream));
-    k_p1_to_p0<<<nbe, kThreads, 0, ctx->stream>>>(g, zl + 3 * fs, out + vlen);
+    k_p1_to_p0<<<nbe, kThreads, 0, ctx->stream>>>(g, zl + 3 * fs, out + vlen, in + vlen, 0.5);
     return launched(ctx);
   };
   // flat CGS passes over composite vectors (k_gs_pass with the composite length)
@@ -1872,14 +1872,14 @@ stk_status stk_p0_solve(stk_ctx* ctx, const double* bu, const double* b0, double
   stk_report* Rp = rep ? rep : &local;
   memset(Rp, 0, sizeof(*Rp));
   double nb2 = 0.0, nr2 = 0.0;
-  ST(gs(GS_DOTS, B, 0, B, nullptr, coef, 1));  // ||b||^2 (slot nv = 0)
+  ST(gs(GS_UPDATE_NORM, B, 0, B, nullptr, coef, 1));  // ||b||^2 (no update with nv = 0, slot 0 = w . w)
   ST(host(coef, 1, &nb2));
   const double bnorm = std::sqrt(nb2);
   auto residual = [&]() -> stk_status {  // R = B - K X, returns ||R||^2 in nr2
     ST(Kop(X, R));
     k_axpby_flat<<<kGsBlocks, 256, 0, ctx->stream>>>(clen, 1.0, B, -1.0, R);
     ST(launched(ctx));
-    ST(gs(GS_DOTS, R, 0, R, nullptr, coef, 1));
+    ST(gs(GS_UPDATE_NORM, R, 0, R, nullptr, coef, 1));
     return host(coef, 1, &nr2);
   };
   ST(residual());
