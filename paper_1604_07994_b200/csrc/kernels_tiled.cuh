@@ -61,6 +61,26 @@ constexpr int FST = ((PLANE + 15) / 16) * 16;
 #endif
 constexpr int PREF = STK_PREF, RING = PREF + 2;
 constexpr int NBAR = STK_DECOUPLE ? 2 * RING : RING;
+// STK_PROD4=1: the four TMA boxes of a plane (u1, u2, u3, p) are issued by lane 0 of
+// warps 0..3, one box each (thread 0 also posts the expect_tx), instead of all four by
+// thread 0: warp 0 no longer runs ~150 extra instructions per plane while the other
+// warps wait for it at the next barrier (ncu: 1.25 barrier-stall cycles per issue).
+// Measured: no gain (apply 391 vs 391 us, velocity pass 411 vs 363 us at cfg3) -- opt-in.
+#ifndef STK_PROD4
+#define STK_PROD4 0
+#endif
+// STK_NR2_MASK bit OP: the stream kernel of that OP gives every thread TWO y-adjacent
+// columns of the tile (NT/2 threads per CTA): the per-plane loop overhead (barrier wait,
+// ring bookkeeping, code / aux prefetch) is paid once per two rows and 8 of the 28
+// staged-point loads are shared between the two columns.  Measured slower (apply 446 vs
+// 391 us at cfg3: 30 % fewer instructions but half the warps per SM) -- opt-in.
+#ifndef STK_NR2_MASK
+#define STK_NR2_MASK 0
+#endif
+#ifndef STK_REGS_NR2
+#define STK_REGS_NR2 168
+#endif
+__host__ __device__ constexpr int nr_of(int op) { return ((STK_NR2_MASK >> op) & 1) ? 2 : 1; }
 // per-row auxiliary fields, prefetched one row ahead by cp.async into a per-thread
 // double buffer: RESID b (4), VEL f (3), P1 g (1), P2 own p (1)
 __host__ __device__ constexpr int n_aux(int op) { return op == 1 ? 4 : op == 2 ? 3 : (op == 3 || op == 4) ? 1 : 0; }
@@ -798,13 +818,15 @@ template <int FORM, int OP>
 #ifndef STK_REGS_P
 #define STK_REGS_P 80
 #endif
-__global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_VEL) ? STK_REGS_AR : STK_REGS_P)
+__global__ void __maxnreg__(nr_of(OP) == 2 ? STK_REGS_NR2 : OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_VEL) ? STK_REGS_AR : STK_REGS_P)
     k_stream(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapP,
              DGrid g,
              StreamArgs a) {
   constexpr int NF = OP == OP_P2 ? 1 : 4;
   constexpr int NA = n_aux(OP);
   constexpr int SLOT = slot_doubles(OP);
+  constexpr int NR = nr_of(OP);    // tile rows (columns of the z-march) per thread
+  constexpr int NTk = NT / NR;     // threads of this CTA
   constexpr uint32_t TX_BYTES = NF * PLANE * sizeof(double);
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* smem_raw =
@@ -831,7 +853,7 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
   if (threadIdx.x == 0) {
     for (int s = 0; s < RING; ++s) mbar_init(&bars[s], 1);
 #if STK_DECOUPLE
-    for (int s = 0; s < RING; ++s) mbar_init(&bars[RING + s], NT / 32);  // "empty": one arrival per warp
+    for (int s = 0; s < RING; ++s) mbar_init(&bars[RING + s], NTk / 32);  // "empty": one arrival per warp
 #endif
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #if STK_TMA_PREFETCH
@@ -849,7 +871,10 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
     const int tkb = g.z0 + (it / tiles) * a.kchunk;
     return min(tkb + a.kchunk, g.z0 + g.nzl) - tkb + 2;
   };
-  if ((STK_DECOUPLE || threadIdx.x == 0) && (int)blockIdx.x < nitems) {
+  // threads that keep the producer sequence: thread 0, or lane 0 of warps 0..NF-1 (STK_PROD4)
+  const bool prod = STK_DECOUPLE || (STK_PROD4 ? ((threadIdx.x & 31) == 0 && (int)(threadIdx.x >> 5) < NF)
+                                               : threadIdx.x == 0);
+  if (prod && (int)blockIdx.x < nitems) {
     pM = item_planes(blockIdx.x);
     pvalid = true;
   }
@@ -863,8 +888,14 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
 #if STK_TMA_FENCE
       fence_proxy_async();
 #endif
-      mbar_expect_tx(&bars[s], TX_BYTES);
       double* dst = ring + s * SLOT;
+#if STK_PROD4 && !STK_DECOUPLE
+      const int w = threadIdx.x >> 5;  // this thread's box: field w (complete_tx may precede the expect_tx)
+      if (w == 0) mbar_expect_tx(&bars[s], TX_BYTES);
+      if (NF == 4 && w < 3) tma_load_4d(dst + w * FST, &mapU, &bars[s], pi0 - 1 - a.ux0, pj0 - 1 - a.uy0, P - a.uz0, w);
+      else tma_load_4d(dst + (NF == 4 ? 3 * FST : 0), &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
+#else
+      mbar_expect_tx(&bars[s], TX_BYTES);
       if (NF == 4) {
         for (int f = 0; f < 3; ++f)
           tma_load_4d(dst + f * FST, &mapU, &bars[s], pi0 - 1 - a.ux0, pj0 - 1 - a.uy0, P - a.uz0, f);
@@ -872,6 +903,7 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
       } else {
         tma_load_4d(dst, &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
       }
+#endif
     }
     ++pS;
     if (++pp == pM) {
@@ -882,13 +914,13 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
       if (pvalid) pM = item_planes(it);
     }
   };
-  if (STK_DECOUPLE || threadIdx.x == 0)
-    for (int q = 0; q < RING - 2; ++q) issue_next(threadIdx.x == 0);  // consumer iteration S stages plane S+RING-2
+  if (prod)
+    for (int q = 0; q < RING - 2; ++q) issue_next(STK_DECOUPLE ? threadIdx.x == 0 : true);  // consumer iteration S stages plane S+RING-2
 
   int S = 0;  // consumer: global plane sequence number
   // debug trace (a.trace != nullptr): cycles in the plane waits, the per-plane
   // barrier and the producer's issue, for thread 0 and for the last warp's lane 0
-  const bool trc = !STK_DECOUPLE && a.trace != nullptr && (threadIdx.x == 0 || threadIdx.x == NT - 32);
+  const bool trc = !STK_DECOUPLE && a.trace != nullptr && (threadIdx.x == 0 || threadIdx.x == NTk - 32);
   unsigned long long tw = 0, ts = 0, ti = 0, t_start = trc ? clock64() : 0;
   auto wait_plane = [&]() -> const double* {
     const int s = S % RING;
@@ -899,7 +931,7 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
   };
   auto release = [&]() {  // all reads of plane S-2 are done: stage a new plane into its slot
 #if STK_DECOUPLE
-    constexpr int NW = NT / 32;
+    constexpr int NW = NTk / 32;
     __syncwarp();
     if (S >= 2 && (threadIdx.x & 31) == 0) mbar_arrive(&bars[RING + (S - 2) % RING]);
     if ((S % NW) == (int)(threadIdx.x >> 5) && pvalid) {
@@ -914,7 +946,7 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
     const unsigned long long c0 = trc ? clock64() : 0;
     __syncthreads();
     const unsigned long long c1 = trc ? clock64() : 0;
-    if (threadIdx.x == 0) issue_next(true);
+    if (prod) issue_next(true);
     if (trc) {
       ts += c1 - c0;
       ti += clock64() - c1;
@@ -922,8 +954,8 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
     ++S;
 #endif
   };
-  const int i_ofs = tx, j_ofs = ty;
-  const int base = (ty + 1) * HX + (tx + 1);
+  const int i_ofs = tx, j_ofs = ty * NR;
+  const int base = (ty * NR + 1) * HX + (tx + 1);   // row r of this thread: base + r HX
 
   for (int it = blockIdx.x; it < nitems; it += G) {
     int i0, j0, kb, M;
@@ -932,79 +964,118 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
     const bool last_x = i0 + TX == g.n, last_y = j0 + TY == g.n;
     const int i = i0 + i_ofs, j = j0 + j_ofs;
     // extra face rows: (n, j) for the last lane of last-x tiles, (i, n) for the
-    // last warp of last-y tiles, (n, n) for the last thread of the corner tile
-    const bool ex_x = last_x && tx == TX - 1, ex_y = last_y && ty == TY - 1, ex_c = ex_x && ex_y;
+    // last row of last-y tiles, (n, n) for the last thread of the corner tile
+    const bool ex_x = last_x && tx == TX - 1, ex_yt = last_y && ty == TY / NR - 1;  // ex_y: its row NR-1
     const bool any_ex = last_x || last_y;
 
     // iteration m (plane P = kb-1+m) uses accumulators (acc0, acc1, acc2) for
     // outputs (P-1, P, P+1); R[] rotates by one per iteration (unrolled by 3)
-    Acc R0, R1, R2;
+    Acc R0[NR], R1[NR], R2[NR];
     // m = 0 (plane kb-1): only output kb (its z-1 plane)
-    R2.zero();
-    accumulate<FORM, OP, -1>(R2, wait_plane(), base);
-    release();
-    // m = 1 (plane kb): outputs kb (in-plane) and kb+1 (z-1 plane)
-    R0.zero();
     {
       const double* pl = wait_plane();
-      accumulate3<FORM, OP, 6>(R0, R2, R0, pl, base);  // R2: in-plane (output kb), R0: output kb+1
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        R2[r].zero();
+        accumulate<FORM, OP, -1>(R2[r], pl, base + r * HX);
+      }
     }
     release();
-    int64_t o = vidx(g, i, j, kb);  // output row of the current iteration
-    uint8_t code_nx = __ldg(g.code + o);
+    // m = 1 (plane kb): outputs kb (in-plane) and kb+1 (z-1 plane)
+    {
+      const double* pl = wait_plane();
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        R0[r].zero();
+        accumulate3<FORM, OP, 6>(R0[r], R2[r], R0[r], pl, base + r * HX);  // R2: in-plane (output kb), R0: output kb+1
+      }
+    }
+    release();
+    int64_t o = vidx(g, i, j, kb);  // output row of the current iteration (row r: o + r px)
+    uint8_t code_nx[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) code_nx[r] = __ldg(g.code + o + r * g.px);
     // aux of row kb into buffer ab (cp.async group); each body prefetches the next row
     const double* auxsrc = OP == OP_P2 ? a.out : a.aux;
     auto aux_issue = [&](int64_t orow, int buf) {
 #pragma unroll
-      for (int f = 0; f < NA; ++f) cp_async8(auxb + (buf * NA + f) * NT + threadIdx.x, auxsrc + f * g.fs + orow);
+      for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int f = 0; f < NA; ++f)
+          cp_async8(auxb + (buf * NA + f) * NT + r * NTk + threadIdx.x, auxsrc + f * g.fs + orow + r * g.px);
       cp_async_commit();
     };
     int ab = 0;
     if (NA > 0) aux_issue(o, ab);
 
-    auto body = [&](int m, Acc& acc0, Acc& acc1, Acc& acc2) {
+    auto body = [&](int m, Acc (&acc0)[NR], Acc (&acc1)[NR], Acc (&acc2)[NR]) {
       const int k = kb1 + m - 1;  // output finished in this iteration
-      acc2.zero();
       // per-output data of row k, staged with plane k (previous slot, landed)
-      const uint8_t code = code_nx;           // loaded one iteration ahead
-      code_nx = __ldg(g.code + o + g.py);     // next row (the code array holds the halo planes)
-      uint8_t cxy[3] = {0xFF, 0xFF, 0xFF};
-      if (any_ex) {
-        if (ex_x) cxy[0] = __ldg(g.code + o + 1);
-        if (ex_y) cxy[1] = __ldg(g.code + o + g.px);
-        if (ex_c) cxy[2] = __ldg(g.code + o + g.px + 1);
+      uint8_t code[NR];
+      uint8_t cxy[NR][3];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        acc2[r].zero();
+        code[r] = code_nx[r];                                 // loaded one iteration ahead
+        code_nx[r] = __ldg(g.code + o + r * g.px + g.py);     // next row (the code array holds the halo planes)
+        cxy[r][0] = cxy[r][1] = cxy[r][2] = 0xFF;
       }
-      double aux[4] = {0, 0, 0, 0};
+      if (any_ex) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const bool ex_y = ex_yt && r == NR - 1;
+          if (ex_x) cxy[r][0] = __ldg(g.code + o + r * g.px + 1);
+          if (ex_y) cxy[r][1] = __ldg(g.code + o + r * g.px + g.px);
+          if (ex_x && ex_y) cxy[r][2] = __ldg(g.code + o + r * g.px + g.px + 1);
+        }
+      }
+      double aux[NR][4];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) aux[r][0] = aux[r][1] = aux[r][2] = aux[r][3] = 0.0;
       if (NA > 0) {
         aux_issue(o + g.py, ab ^ 1);  // next row (the slab holds the halo planes)
         cp_async_wait1();             // this row's group has landed
 #pragma unroll
-        for (int f = 0; f < NA; ++f) aux[OP == OP_RESID || OP == OP_VEL ? f : 3] = auxb[(ab * NA + f) * NT + threadIdx.x];
+        for (int r = 0; r < NR; ++r)
+#pragma unroll
+          for (int f = 0; f < NA; ++f)
+            aux[r][OP == OP_RESID || OP == OP_VEL ? f : 3] = auxb[(ab * NA + f) * NT + r * NTk + threadIdx.x];
         ab ^= 1;
       }
       const double* pl = wait_plane();
       // plane P is output P-1's z+1 plane, output P's own plane, output P+1's z-1 plane
-      if (m < M - 1) accumulate3<FORM, OP, 7>(acc0, acc1, acc2, pl, base);
-      else accumulate3<FORM, OP, 1>(acc0, acc1, acc2, pl, base);
-      const double* pls[3] = {ring + ((S + RING - 2) % RING) * SLOT, ring + ((S + RING - 1) % RING) * SLOT, pl};
-      if (!(code & (0x80 | CODE_TOP))) {
-        finish_row<FORM, OP>(g, a, i, j, k, o, code, aux, acc0, pls, base);
-      } else if (code != CODE_IRREGULAR && !(OP == OP_VEL && a.inplace)) {
-        finish_top<FORM, OP>(g, a, i, j, k, o, code, aux, pls, base);
+      if (m < M - 1) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) accumulate3<FORM, OP, 7>(acc0[r], acc1[r], acc2[r], pl, base + r * HX);
+      } else {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) accumulate3<FORM, OP, 1>(acc0[r], acc1[r], acc2[r], pl, base + r * HX);
       }
-      // face rows i = n, j = n (Dirichlet with an isoviscous star, else list rows)
-      if (any_ex) {
-        if (ex_x && !(cxy[0] & 0x80)) {
-          const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, false>(pls, base + 1);
-          finish_boundary<OP>(g, a, g.n, j, k, cxy[0], Bu, pls, base + 1);
+      const double* pls[3] = {ring + ((S + RING - 2) % RING) * SLOT, ring + ((S + RING - 1) % RING) * SLOT, pl};
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int br = base + r * HX, jr = j + r;
+        const int64_t orr = o + r * g.px;
+        if (!(code[r] & (0x80 | CODE_TOP))) {
+          finish_row<FORM, OP>(g, a, i, jr, k, orr, code[r], aux[r], acc0[r], pls, br);
+        } else if (code[r] != CODE_IRREGULAR && !(OP == OP_VEL && a.inplace)) {
+          finish_top<FORM, OP>(g, a, i, jr, k, orr, code[r], aux[r], pls, br);
         }
-        if (ex_y && !(cxy[1] & 0x80)) {
-          const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<false, true>(pls, base + HX);
-          finish_boundary<OP>(g, a, i, g.n, k, cxy[1], Bu, pls, base + HX);
-        }
-        if (ex_c && !(cxy[2] & 0x80)) {
-          const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, true>(pls, base + HX + 1);
-          finish_boundary<OP>(g, a, g.n, g.n, k, cxy[2], Bu, pls, base + HX + 1);
+        // face rows i = n, j = n (Dirichlet with an isoviscous star, else list rows)
+        if (any_ex) {
+          const bool ex_y = ex_yt && r == NR - 1;
+          if (ex_x && !(cxy[r][0] & 0x80)) {
+            const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, false>(pls, br + 1);
+            finish_boundary<OP>(g, a, g.n, jr, k, cxy[r][0], Bu, pls, br + 1);
+          }
+          if (ex_y && !(cxy[r][1] & 0x80)) {
+            const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<false, true>(pls, br + HX);
+            finish_boundary<OP>(g, a, i, g.n, k, cxy[r][1], Bu, pls, br + HX);
+          }
+          if (ex_x && ex_y && !(cxy[r][2] & 0x80)) {
+            const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, true>(pls, br + HX + 1);
+            finish_boundary<OP>(g, a, g.n, g.n, k, cxy[r][2], Bu, pls, br + HX + 1);
+          }
         }
       }
       release();
@@ -1013,14 +1084,17 @@ __global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_V
 #ifndef STK_UNROLL3_MASK
 #define STK_UNROLL3_MASK (1 << OP_VEL)
 #endif
-    if constexpr (!((STK_UNROLL3_MASK >> OP) & 1)) {
+    if constexpr (!((STK_UNROLL3_MASK >> OP) & 1) || NR > 1) {
       // one body instance, the accumulators rotate by register moves: 3x less code
       // (measured faster for these OPs; the velocity pass keeps the 3-way unroll)
 #pragma unroll 1
       for (int m = 2; m < M; ++m) {
         body(m, R2, R0, R1);
-        R2 = R0;
-        R0 = R1;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          R2[r] = R0[r];
+          R0[r] = R1[r];
+        }
       }
     } else {
       int m = 2;
@@ -1163,7 +1237,7 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
     int per_sm = 0, nsm = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream<FORM, OP>, NT, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream<FORM, OP>, NT / nr_of(OP), sm);
     slots = std::max(1, nsm * std::max(1, per_sm));
   }
   // chunk length: >= ~4 items per CTA for balance, 4..16 planes (short chunks keep
@@ -1190,7 +1264,7 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
   static unsigned long long* tbuf = nullptr;
   if (trace && !tbuf) cudaMallocManaged(&tbuf, sizeof(unsigned long long) * 4096 * 10);
   a.trace = trace ? tbuf : nullptr;
-  k_stream<FORM, OP><<<dim3(grid), NT, sm, st>>>(mU, mP, g, a);
+  k_stream<FORM, OP><<<dim3(grid), NT / nr_of(OP), sm, st>>>(mU, mP, g, a);
   if (trace) {  // debug: mean per-CTA cycle split of this launch
     cudaStreamSynchronize(st);
     double tot[2][5] = {};
