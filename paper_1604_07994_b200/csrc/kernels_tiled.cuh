@@ -48,39 +48,20 @@ constexpr int TX = 32, TY = 8, NT = TX * TY;
 constexpr int HX = TX + 2, HY = TY + 2, PLANE = HX * HY;
 // shared-memory stride of one staged field plane: 128-byte aligned TMA destinations
 constexpr int FST = ((PLANE + 15) / 16) * 16;
-#ifndef STK_PREF
-#define STK_PREF 3
+constexpr int PREF = 3, RING = PREF + 2;
+// STK_MU_SMEM=1: the per-class (mu, 1/mu) table is copied to shared memory at kernel
+// start; the row finish reads it from there (a ~30-cycle LDS) instead of two dependent
+// global loads behind the code byte (ncu: 0.6-2.0 long-scoreboard stall cycles per issue).
+#ifndef STK_MU_SMEM
+#define STK_MU_SMEM 0
 #endif
-// STK_DECOUPLE=1: no per-plane __syncthreads.  Every warp releases plane S-2 on a
-// per-slot "empty" mbarrier (one arrival per warp) and runs on; the warp S % NW waits
-// for that barrier and stages plane S+RING-2 (the producer role rotates over the warps),
-// so the warps of a CTA drift up to PREF planes apart and their shared-memory, fp64 and
-// store phases overlap instead of running in lockstep.
-#ifndef STK_DECOUPLE
-#define STK_DECOUPLE 0
+__device__ __forceinline__ double tab_ld(const double* mt, int idx) {
+#if STK_MU_SMEM
+  return mt[idx];
+#else
+  return __ldg(mt + idx);
 #endif
-constexpr int PREF = STK_PREF, RING = PREF + 2;
-constexpr int NBAR = STK_DECOUPLE ? 2 * RING : RING;
-// STK_PROD4=1: the four TMA boxes of a plane (u1, u2, u3, p) are issued by lane 0 of
-// warps 0..3, one box each (thread 0 also posts the expect_tx), instead of all four by
-// thread 0: warp 0 no longer runs ~150 extra instructions per plane while the other
-// warps wait for it at the next barrier (ncu: 1.25 barrier-stall cycles per issue).
-// Measured: no gain (apply 391 vs 391 us, velocity pass 411 vs 363 us at cfg3) -- opt-in.
-#ifndef STK_PROD4
-#define STK_PROD4 0
-#endif
-// STK_NR2_MASK bit OP: the stream kernel of that OP gives every thread TWO y-adjacent
-// columns of the tile (NT/2 threads per CTA): the per-plane loop overhead (barrier wait,
-// ring bookkeeping, code / aux prefetch) is paid once per two rows and 8 of the 28
-// staged-point loads are shared between the two columns.  Measured slower (apply 446 vs
-// 391 us at cfg3: 30 % fewer instructions but half the warps per SM) -- opt-in.
-#ifndef STK_NR2_MASK
-#define STK_NR2_MASK 0
-#endif
-#ifndef STK_REGS_NR2
-#define STK_REGS_NR2 168
-#endif
-__host__ __device__ constexpr int nr_of(int op) { return ((STK_NR2_MASK >> op) & 1) ? 2 : 1; }
+}
 // per-row auxiliary fields, prefetched one row ahead by cp.async into a per-thread
 // double buffer: RESID b (4), VEL f (3), P1 g (1), P2 own p (1)
 __host__ __device__ constexpr int n_aux(int op) { return op == 1 ? 4 : op == 2 ? 3 : (op == 3 || op == 4) ? 1 : 0; }
@@ -241,9 +222,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -465,13 +443,14 @@ __device__ __forceinline__ double b_row_smem(const double* const pl[3], int s) {
 // = k-1, k, k+1 (4-field slots, or 1-field T slots for P2), s = smem position
 template <int OP>
 __device__ __forceinline__ void finish_boundary(const DGrid& g, const StreamArgs& a, int i, int j, int k,
-                                                uint8_t code, double Bu, const double* const pl[3], int s) {
+                                                uint8_t code, double Bu, const double* const pl[3], int s,
+                                                const double* mt) {
   const int64_t o = vidx(g, i, j, k);
   const double h = g.h;
   constexpr int PF = OP == OP_P2 ? 0 : 3;  // pressure (or T) field within a slot
   double sum, diag;
   c_trunc(pl[0] + PF * FST, pl[1] + PF * FST, pl[2] + PF * FST, s, i, j, k, g.n, sum, diag);
-  const double cw = g.delta * h * h * h * imu_of(g, code) * (1.0 / 6.0);  // per-count edge weight
+  const double cw = g.delta * h * h * h * tab_ld(mt, 256 + code) * (1.0 / 6.0);  // per-count edge weight
   const double pv = pl[1][PF * FST + s];
   if (OP == OP_APPLY || OP == OP_RESID) {
     const unsigned blk = OP == OP_APPLY ? a.blocks : BLK_ALL;
@@ -713,13 +692,14 @@ __device__ __forceinline__ void top_plane(Acc& acc, const double* const pls[3], 
 // from the staged planes k-1 (pls[0]) and k (pls[1])
 template <int FORM, int OP>
 __device__ __forceinline__ void finish_top(const DGrid& g, const StreamArgs& a, int i, int j, int k, int64_t o,
-                                        uint8_t code, const double aux[4], const double* const pls[3], int base) {
+                                        uint8_t code, const double aux[4], const double* const pls[3], int base,
+                                        const double* mt) {
   Acc acc;
   acc.zero();
   top_plane<FORM, OP, -1>(acc, pls, base);
   top_plane<FORM, OP, 0>(acc, pls, base);
   const int cl = code & (CODE_TOP - 1);
-  const double h = g.h, mu = mu_of(g, cl), imu = imu_of(g, cl);
+  const double h = g.h, mu = tab_ld(mt, cl), imu = tab_ld(mt, 256 + cl);
   const double sA = mu * h * (1.0 / 6.0), sB = h * h * (1.0 / 24.0), sC = g.delta * h * h * h * imu * (1.0 / 6.0);
   constexpr double kAd0 = KT<0, FORM, 0, 0, 0, 0, 0>::v, kAd1 = KT<0, FORM, 1, 1, 0, 0, 0>::v,
                    kAd2 = KT<0, FORM, 2, 2, 0, 0, 0>::v, kCd = KT<3, 0, 0, 0, 0, 0, 0>::v;
@@ -757,13 +737,13 @@ __device__ __forceinline__ void finish_top(const DGrid& g, const StreamArgs& a, 
 template <int FORM, int OP>
 __device__ __forceinline__ void finish_row(const DGrid& g, const StreamArgs& a, int i, int j, int k, int64_t o,
                                            uint8_t code, const double aux[4], const Acc& acc,
-                                           const double* const pls[3], int base) {
+                                           const double* const pls[3], int base, const double* mt) {
   const double h = g.h;
   if (!(i > 0 && j > 0 && k > 0 && k < g.n)) {
-    finish_boundary<OP>(g, a, i, j, k, code, acc.B, pls, base);
+    finish_boundary<OP>(g, a, i, j, k, code, acc.B, pls, base, mt);
     return;
   }
-  const double mu = mu_of(g, code), imu = imu_of(g, code);
+  const double mu = tab_ld(mt, code), imu = tab_ld(mt, 256 + code);
   const double sA = mu * h * (1.0 / 6.0);                       // 6A units
   const double sB = h * h * (1.0 / 24.0);                       // 24B, 24B^T units
   const double sC = g.delta * h * h * h * imu * (1.0 / 6.0);    // 6C units
@@ -818,22 +798,20 @@ template <int FORM, int OP>
 #ifndef STK_REGS_P
 #define STK_REGS_P 80
 #endif
-__global__ void __maxnreg__(nr_of(OP) == 2 ? STK_REGS_NR2 : OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_VEL) ? STK_REGS_AR : STK_REGS_P)
+__global__ void __maxnreg__(OP == OP_RESID ? 128 : (OP == OP_APPLY || OP == OP_VEL) ? STK_REGS_AR : STK_REGS_P)
     k_stream(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapP,
              DGrid g,
              StreamArgs a) {
   constexpr int NF = OP == OP_P2 ? 1 : 4;
   constexpr int NA = n_aux(OP);
   constexpr int SLOT = slot_doubles(OP);
-  constexpr int NR = nr_of(OP);    // tile rows (columns of the z-march) per thread
-  constexpr int NTk = NT / NR;     // threads of this CTA
   constexpr uint32_t TX_BYTES = NF * PLANE * sizeof(double);
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* smem_raw =
       smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);  // 1 KB aligned TMA destinations
   double* ring = reinterpret_cast<double*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + RING * SLOT * sizeof(double));
-  double* auxb = reinterpret_cast<double*>(bars + NBAR);  // [2][NA][NT] per-thread aux double buffer
+  double* auxb = reinterpret_cast<double*>(bars + RING);  // [2][NA][NT] per-thread aux double buffer
 
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int ntx = g.n / TX;
@@ -850,11 +828,15 @@ __global__ void __maxnreg__(nr_of(OP) == 2 ? STK_REGS_NR2 : OP == OP_RESID ? 128
     tM = min(tkb + a.kchunk, g.z0 + g.nzl) - tkb + 2;
   };
 
+#if STK_MU_SMEM
+  __shared__ double s_mt[512];  // per-class mu [0..255] and 1/mu [256..511]
+  for (int c = threadIdx.x; c < 512; c += NT) s_mt[c] = __ldg(g.mu + c);
+  const double* mt = s_mt;
+#else
+  const double* mt = g.mu;
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < RING; ++s) mbar_init(&bars[s], 1);
-#if STK_DECOUPLE
-    for (int s = 0; s < RING; ++s) mbar_init(&bars[RING + s], NTk / 32);  // "empty": one arrival per warp
-#endif
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #if STK_TMA_PREFETCH
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapU) : "memory");
@@ -862,48 +844,29 @@ __global__ void __maxnreg__(nr_of(OP) == 2 ? STK_REGS_NR2 : OP == OP_RESID ? 128
 #endif
   }
   __syncthreads();
-  // Producer: the planes of this CTA's items, items blockIdx.x + q G, back to back;
-  // global plane sequence number S selects slot S % RING.  The sequence state is kept
-  // by thread 0 (or, STK_DECOUPLE, by every thread: the issuing warp rotates).
-  int pq = 0, pp = 0, pS = 0, pM = 0;   // item counter, plane within the item, sequence number, planes of the item
+  // Producer (thread 0): the planes of this CTA's items, items blockIdx.x + q G,
+  // back to back; global plane sequence number S selects slot S % RING.
+  int pq = 0, pp = 0, pS = 0, pi0 = 0, pj0 = 0, pkb = 0, pM = 0;
   bool pvalid = false;
-  auto item_planes = [&](int it) {
-    const int tkb = g.z0 + (it / tiles) * a.kchunk;
-    return min(tkb + a.kchunk, g.z0 + g.nzl) - tkb + 2;
-  };
-  // threads that keep the producer sequence: thread 0, or lane 0 of warps 0..NF-1 (STK_PROD4)
-  const bool prod = STK_DECOUPLE || (STK_PROD4 ? ((threadIdx.x & 31) == 0 && (int)(threadIdx.x >> 5) < NF)
-                                               : threadIdx.x == 0);
-  if (prod && (int)blockIdx.x < nitems) {
-    pM = item_planes(blockIdx.x);
+  if (threadIdx.x == 0 && (int)blockIdx.x < nitems) {
+    item_geom(blockIdx.x, pi0, pj0, pkb, pM);
     pvalid = true;
   }
-  auto issue_next = [&](bool do_issue) {  // stage the next plane of the sequence (do_issue: this thread issues)
+  auto issue_next = [&]() {  // thread 0: stage the next plane of the sequence
     if (!pvalid) return;
-    if (do_issue) {
-      int pi0, pj0, pkb, pMM;
-      item_geom(blockIdx.x + pq * G, pi0, pj0, pkb, pMM);
-      const int s = pS % RING;
-      const int P = pkb - 1 + pp;
+    const int s = pS % RING;
+    const int P = pkb - 1 + pp;
 #if STK_TMA_FENCE
-      fence_proxy_async();
+    fence_proxy_async();
 #endif
-      double* dst = ring + s * SLOT;
-#if STK_PROD4 && !STK_DECOUPLE
-      const int w = threadIdx.x >> 5;  // this thread's box: field w (complete_tx may precede the expect_tx)
-      if (w == 0) mbar_expect_tx(&bars[s], TX_BYTES);
-      if (NF == 4 && w < 3) tma_load_4d(dst + w * FST, &mapU, &bars[s], pi0 - 1 - a.ux0, pj0 - 1 - a.uy0, P - a.uz0, w);
-      else tma_load_4d(dst + (NF == 4 ? 3 * FST : 0), &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
-#else
-      mbar_expect_tx(&bars[s], TX_BYTES);
-      if (NF == 4) {
-        for (int f = 0; f < 3; ++f)
-          tma_load_4d(dst + f * FST, &mapU, &bars[s], pi0 - 1 - a.ux0, pj0 - 1 - a.uy0, P - a.uz0, f);
-        tma_load_4d(dst + 3 * FST, &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
-      } else {
-        tma_load_4d(dst, &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
-      }
-#endif
+    mbar_expect_tx(&bars[s], TX_BYTES);
+    double* dst = ring + s * SLOT;
+    if (NF == 4) {
+      for (int f = 0; f < 3; ++f)
+        tma_load_4d(dst + f * FST, &mapU, &bars[s], pi0 - 1 - a.ux0, pj0 - 1 - a.uy0, P - a.uz0, f);
+      tma_load_4d(dst + 3 * FST, &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
+    } else {
+      tma_load_4d(dst, &mapP, &bars[s], pi0, pj0, P - g.z0 + 1, 0);
     }
     ++pS;
     if (++pp == pM) {
@@ -911,16 +874,16 @@ __global__ void __maxnreg__(nr_of(OP) == 2 ? STK_REGS_NR2 : OP == OP_RESID ? 128
       ++pq;
       const int it = blockIdx.x + pq * G;
       pvalid = it < nitems;
-      if (pvalid) pM = item_planes(it);
+      if (pvalid) item_geom(it, pi0, pj0, pkb, pM);
     }
   };
-  if (prod)
-    for (int q = 0; q < RING - 2; ++q) issue_next(STK_DECOUPLE ? threadIdx.x == 0 : true);  // consumer iteration S stages plane S+RING-2
+  if (threadIdx.x == 0)
+    for (int q = 0; q < RING - 2; ++q) issue_next();  // consumer iteration S stages plane S+RING-2
 
   int S = 0;  // consumer: global plane sequence number
   // debug trace (a.trace != nullptr): cycles in the plane waits, the per-plane
   // barrier and the producer's issue, for thread 0 and for the last warp's lane 0
-  const bool trc = !STK_DECOUPLE && a.trace != nullptr && (threadIdx.x == 0 || threadIdx.x == NTk - 32);
+  const bool trc = a.trace != nullptr && (threadIdx.x == 0 || threadIdx.x == NT - 32);
   unsigned long long tw = 0, ts = 0, ti = 0, t_start = trc ? clock64() : 0;
   auto wait_plane = [&]() -> const double* {
     const int s = S % RING;
@@ -930,32 +893,18 @@ __global__ void __maxnreg__(nr_of(OP) == 2 ? STK_REGS_NR2 : OP == OP_RESID ? 128
     return ring + s * SLOT;
   };
   auto release = [&]() {  // all reads of plane S-2 are done: stage a new plane into its slot
-#if STK_DECOUPLE
-    constexpr int NW = NTk / 32;
-    __syncwarp();
-    if (S >= 2 && (threadIdx.x & 31) == 0) mbar_arrive(&bars[RING + (S - 2) % RING]);
-    if ((S % NW) == (int)(threadIdx.x >> 5) && pvalid) {
-      // this warp's turn: every warp has released plane S-2 (slot of plane S+RING-2)
-      if (S >= 2) mbar_wait(&bars[RING + (S - 2) % RING], ((S - 2) / RING) & 1);
-      issue_next((threadIdx.x & 31) == 0);
-    } else {
-      issue_next(false);
-    }
-    ++S;
-#else
     const unsigned long long c0 = trc ? clock64() : 0;
     __syncthreads();
     const unsigned long long c1 = trc ? clock64() : 0;
-    if (prod) issue_next(true);
+    if (threadIdx.x == 0) issue_next();
     if (trc) {
       ts += c1 - c0;
       ti += clock64() - c1;
     }
     ++S;
-#endif
   };
-  const int i_ofs = tx, j_ofs = ty * NR;
-  const int base = (ty * NR + 1) * HX + (tx + 1);   // row r of this thread: base + r HX
+  const int i_ofs = tx, j_ofs = ty;
+  const int base = (ty + 1) * HX + (tx + 1);
 
   for (int it = blockIdx.x; it < nitems; it += G) {
     int i0, j0, kb, M;
@@ -964,118 +913,79 @@ __global__ void __maxnreg__(nr_of(OP) == 2 ? STK_REGS_NR2 : OP == OP_RESID ? 128
     const bool last_x = i0 + TX == g.n, last_y = j0 + TY == g.n;
     const int i = i0 + i_ofs, j = j0 + j_ofs;
     // extra face rows: (n, j) for the last lane of last-x tiles, (i, n) for the
-    // last row of last-y tiles, (n, n) for the last thread of the corner tile
-    const bool ex_x = last_x && tx == TX - 1, ex_yt = last_y && ty == TY / NR - 1;  // ex_y: its row NR-1
+    // last warp of last-y tiles, (n, n) for the last thread of the corner tile
+    const bool ex_x = last_x && tx == TX - 1, ex_y = last_y && ty == TY - 1, ex_c = ex_x && ex_y;
     const bool any_ex = last_x || last_y;
 
     // iteration m (plane P = kb-1+m) uses accumulators (acc0, acc1, acc2) for
     // outputs (P-1, P, P+1); R[] rotates by one per iteration (unrolled by 3)
-    Acc R0[NR], R1[NR], R2[NR];
+    Acc R0, R1, R2;
     // m = 0 (plane kb-1): only output kb (its z-1 plane)
-    {
-      const double* pl = wait_plane();
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        R2[r].zero();
-        accumulate<FORM, OP, -1>(R2[r], pl, base + r * HX);
-      }
-    }
+    R2.zero();
+    accumulate<FORM, OP, -1>(R2, wait_plane(), base);
     release();
     // m = 1 (plane kb): outputs kb (in-plane) and kb+1 (z-1 plane)
+    R0.zero();
     {
       const double* pl = wait_plane();
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        R0[r].zero();
-        accumulate3<FORM, OP, 6>(R0[r], R2[r], R0[r], pl, base + r * HX);  // R2: in-plane (output kb), R0: output kb+1
-      }
+      accumulate3<FORM, OP, 6>(R0, R2, R0, pl, base);  // R2: in-plane (output kb), R0: output kb+1
     }
     release();
-    int64_t o = vidx(g, i, j, kb);  // output row of the current iteration (row r: o + r px)
-    uint8_t code_nx[NR];
-#pragma unroll
-    for (int r = 0; r < NR; ++r) code_nx[r] = __ldg(g.code + o + r * g.px);
+    int64_t o = vidx(g, i, j, kb);  // output row of the current iteration
+    uint8_t code_nx = __ldg(g.code + o);
     // aux of row kb into buffer ab (cp.async group); each body prefetches the next row
     const double* auxsrc = OP == OP_P2 ? a.out : a.aux;
     auto aux_issue = [&](int64_t orow, int buf) {
 #pragma unroll
-      for (int r = 0; r < NR; ++r)
-#pragma unroll
-        for (int f = 0; f < NA; ++f)
-          cp_async8(auxb + (buf * NA + f) * NT + r * NTk + threadIdx.x, auxsrc + f * g.fs + orow + r * g.px);
+      for (int f = 0; f < NA; ++f) cp_async8(auxb + (buf * NA + f) * NT + threadIdx.x, auxsrc + f * g.fs + orow);
       cp_async_commit();
     };
     int ab = 0;
     if (NA > 0) aux_issue(o, ab);
 
-    auto body = [&](int m, Acc (&acc0)[NR], Acc (&acc1)[NR], Acc (&acc2)[NR]) {
+    auto body = [&](int m, Acc& acc0, Acc& acc1, Acc& acc2) {
       const int k = kb1 + m - 1;  // output finished in this iteration
+      acc2.zero();
       // per-output data of row k, staged with plane k (previous slot, landed)
-      uint8_t code[NR];
-      uint8_t cxy[NR][3];
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        acc2[r].zero();
-        code[r] = code_nx[r];                                 // loaded one iteration ahead
-        code_nx[r] = __ldg(g.code + o + r * g.px + g.py);     // next row (the code array holds the halo planes)
-        cxy[r][0] = cxy[r][1] = cxy[r][2] = 0xFF;
-      }
+      const uint8_t code = code_nx;           // loaded one iteration ahead
+      code_nx = __ldg(g.code + o + g.py);     // next row (the code array holds the halo planes)
+      uint8_t cxy[3] = {0xFF, 0xFF, 0xFF};
       if (any_ex) {
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          const bool ex_y = ex_yt && r == NR - 1;
-          if (ex_x) cxy[r][0] = __ldg(g.code + o + r * g.px + 1);
-          if (ex_y) cxy[r][1] = __ldg(g.code + o + r * g.px + g.px);
-          if (ex_x && ex_y) cxy[r][2] = __ldg(g.code + o + r * g.px + g.px + 1);
-        }
+        if (ex_x) cxy[0] = __ldg(g.code + o + 1);
+        if (ex_y) cxy[1] = __ldg(g.code + o + g.px);
+        if (ex_c) cxy[2] = __ldg(g.code + o + g.px + 1);
       }
-      double aux[NR][4];
-#pragma unroll
-      for (int r = 0; r < NR; ++r) aux[r][0] = aux[r][1] = aux[r][2] = aux[r][3] = 0.0;
+      double aux[4] = {0, 0, 0, 0};
       if (NA > 0) {
         aux_issue(o + g.py, ab ^ 1);  // next row (the slab holds the halo planes)
         cp_async_wait1();             // this row's group has landed
 #pragma unroll
-        for (int r = 0; r < NR; ++r)
-#pragma unroll
-          for (int f = 0; f < NA; ++f)
-            aux[r][OP == OP_RESID || OP == OP_VEL ? f : 3] = auxb[(ab * NA + f) * NT + r * NTk + threadIdx.x];
+        for (int f = 0; f < NA; ++f) aux[OP == OP_RESID || OP == OP_VEL ? f : 3] = auxb[(ab * NA + f) * NT + threadIdx.x];
         ab ^= 1;
       }
       const double* pl = wait_plane();
       // plane P is output P-1's z+1 plane, output P's own plane, output P+1's z-1 plane
-      if (m < M - 1) {
-#pragma unroll
-        for (int r = 0; r < NR; ++r) accumulate3<FORM, OP, 7>(acc0[r], acc1[r], acc2[r], pl, base + r * HX);
-      } else {
-#pragma unroll
-        for (int r = 0; r < NR; ++r) accumulate3<FORM, OP, 1>(acc0[r], acc1[r], acc2[r], pl, base + r * HX);
-      }
+      if (m < M - 1) accumulate3<FORM, OP, 7>(acc0, acc1, acc2, pl, base);
+      else accumulate3<FORM, OP, 1>(acc0, acc1, acc2, pl, base);
       const double* pls[3] = {ring + ((S + RING - 2) % RING) * SLOT, ring + ((S + RING - 1) % RING) * SLOT, pl};
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const int br = base + r * HX, jr = j + r;
-        const int64_t orr = o + r * g.px;
-        if (!(code[r] & (0x80 | CODE_TOP))) {
-          finish_row<FORM, OP>(g, a, i, jr, k, orr, code[r], aux[r], acc0[r], pls, br);
-        } else if (code[r] != CODE_IRREGULAR && !(OP == OP_VEL && a.inplace)) {
-          finish_top<FORM, OP>(g, a, i, jr, k, orr, code[r], aux[r], pls, br);
+      if (!(code & (0x80 | CODE_TOP))) {
+        finish_row<FORM, OP>(g, a, i, j, k, o, code, aux, acc0, pls, base, mt);
+      } else if (code != CODE_IRREGULAR && !(OP == OP_VEL && a.inplace)) {
+        finish_top<FORM, OP>(g, a, i, j, k, o, code, aux, pls, base, mt);
+      }
+      // face rows i = n, j = n (Dirichlet with an isoviscous star, else list rows)
+      if (any_ex) {
+        if (ex_x && !(cxy[0] & 0x80)) {
+          const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, false>(pls, base + 1);
+          finish_boundary<OP>(g, a, g.n, j, k, cxy[0], Bu, pls, base + 1, mt);
         }
-        // face rows i = n, j = n (Dirichlet with an isoviscous star, else list rows)
-        if (any_ex) {
-          const bool ex_y = ex_yt && r == NR - 1;
-          if (ex_x && !(cxy[r][0] & 0x80)) {
-            const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, false>(pls, br + 1);
-            finish_boundary<OP>(g, a, g.n, jr, k, cxy[r][0], Bu, pls, br + 1);
-          }
-          if (ex_y && !(cxy[r][1] & 0x80)) {
-            const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<false, true>(pls, br + HX);
-            finish_boundary<OP>(g, a, i, g.n, k, cxy[r][1], Bu, pls, br + HX);
-          }
-          if (ex_x && ex_y && !(cxy[r][2] & 0x80)) {
-            const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, true>(pls, br + HX + 1);
-            finish_boundary<OP>(g, a, g.n, g.n, k, cxy[r][2], Bu, pls, br + HX + 1);
-          }
+        if (ex_y && !(cxy[1] & 0x80)) {
+          const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<false, true>(pls, base + HX);
+          finish_boundary<OP>(g, a, i, g.n, k, cxy[1], Bu, pls, base + HX, mt);
+        }
+        if (ex_c && !(cxy[2] & 0x80)) {
+          const double Bu = (OP == OP_P2 || OP == OP_VEL) ? 0.0 : b_row_smem<true, true>(pls, base + HX + 1);
+          finish_boundary<OP>(g, a, g.n, g.n, k, cxy[2], Bu, pls, base + HX + 1, mt);
         }
       }
       release();
@@ -1084,17 +994,14 @@ __global__ void __maxnreg__(nr_of(OP) == 2 ? STK_REGS_NR2 : OP == OP_RESID ? 128
 #ifndef STK_UNROLL3_MASK
 #define STK_UNROLL3_MASK (1 << OP_VEL)
 #endif
-    if constexpr (!((STK_UNROLL3_MASK >> OP) & 1) || NR > 1) {
+    if constexpr (!((STK_UNROLL3_MASK >> OP) & 1)) {
       // one body instance, the accumulators rotate by register moves: 3x less code
       // (measured faster for these OPs; the velocity pass keeps the 3-way unroll)
 #pragma unroll 1
       for (int m = 2; m < M; ++m) {
         body(m, R2, R0, R1);
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          R2[r] = R0[r];
-          R0[r] = R1[r];
-        }
+        R2 = R0;
+        R0 = R1;
       }
     } else {
       int m = 2;
@@ -1191,7 +1098,7 @@ inline bool assemble_stencils(cudaStream_t st) {
 }
 
 inline size_t stream_smem(int op) {
-  return 1024 + RING * slot_doubles(op) * sizeof(double) + NBAR * sizeof(uint64_t) + 2 * n_aux(op) * NT * sizeof(double);
+  return 1024 + RING * slot_doubles(op) * sizeof(double) + RING * sizeof(uint64_t) + 2 * n_aux(op) * NT * sizeof(double);
 }
 
 // the irregular-row list of a level (built by stk_assemble)
@@ -1237,7 +1144,7 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
     int per_sm = 0, nsm = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream<FORM, OP>, NT / nr_of(OP), sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stream<FORM, OP>, NT, sm);
     slots = std::max(1, nsm * std::max(1, per_sm));
   }
   // chunk length: >= ~4 items per CTA for balance, 4..16 planes (short chunks keep
@@ -1264,7 +1171,7 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
   static unsigned long long* tbuf = nullptr;
   if (trace && !tbuf) cudaMallocManaged(&tbuf, sizeof(unsigned long long) * 4096 * 10);
   a.trace = trace ? tbuf : nullptr;
-  k_stream<FORM, OP><<<dim3(grid), NT / nr_of(OP), sm, st>>>(mU, mP, g, a);
+  k_stream<FORM, OP><<<dim3(grid), NT, sm, st>>>(mU, mP, g, a);
   if (trace) {  // debug: mean per-CTA cycle split of this launch
     cudaStreamSynchronize(st);
     double tot[2][5] = {};
