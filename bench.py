@@ -111,14 +111,23 @@ def measured_peaks():
 class Clocks:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
+    # one sampler process for the whole run, started before the warm-up (its NVML start-up
+    # stalled the first timed step by some 100 ms on some boxes when started right before
+    # it); only the samples stamped inside the timed region are kept
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,timestamp")
 
     def __init__(self, dev):
         self.dev = dev
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.p = None
+        self.t0 = None
+
+    def mark(self):
+        """The timed region starts now."""
+        import datetime
+        self.t0 = datetime.datetime.now()
 
     def start(self):
         try:
@@ -143,6 +152,16 @@ class Clocks:
                 parts = [x.strip() for x in line.split(",")]
                 if len(parts) >= 9:
                     rows.append(parts)
+        if self.t0 is not None:
+            import datetime
+            inside = []
+            for r in rows:
+                try:
+                    if datetime.datetime.strptime(r[9], "%Y/%m/%d %H:%M:%S.%f") >= self.t0:
+                        inside.append(r)
+                except (ValueError, IndexError):
+                    inside.append(r)
+            rows = inside or rows
         os.unlink(self.f.name)
         if not rows:
             return None
@@ -359,7 +378,9 @@ def run_ours(args, cfg, world, rank, local):
         _, rep = ctx.solve(b, x, rtol=RTOL, max_cycles=args.max_cycles)
         return rep
 
-    # warm-up
+    # warm-up (the clock sampler starts here, its samples count from the timed region on)
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.warmup):
         flush.zero_()
         rep = step()
@@ -367,11 +388,10 @@ def run_ours(args, cfg, world, rank, local):
     log(f"warm-up done: cycles {rep.cycles} rho {rep.rho:.3f} rel {rep.rel_res:.2e}")
 
     # timed steps (device time, CUDA events on the solver stream), library profiling off
-    clocks = Clocks(local)
     l0 = ctx.launch_count()
     ev = []
     reps = []
-    clocks.start()
+    clocks.mark()
     for _ in range(args.steps):
         flush.zero_()                       # L2 flushed between steps (outside the events)
         barrier(world)
@@ -503,6 +523,7 @@ def run_ours(args, cfg, world, rank, local):
     if rank == 0:
         line = {"metric": METRIC, "value": ms * 1e-3 / dofs, "unit": "s/DoF", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+                "step_ms": [round(t, 3) for t in step_ms],
                 "higher_is_better": False, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
                 "config": {"workload": workload_name(cfg.name), "n": cfg.n,
