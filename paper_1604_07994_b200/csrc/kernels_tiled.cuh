@@ -1149,6 +1149,8 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
   }
   // chunk length: >= ~4 items per CTA for balance, 4..16 planes (short chunks keep
   // concurrently streaming neighbour tiles at the same height: halos shared in L2)
+  // (measured, profiles/r02_stream_kchunk_sweep.log: 16 planes is within 1 % of the best at
+  // n = 256; 32 planes win 3 % per kernel at n = 512 but are not adopted, see DESIGN 8)
   const int want = std::max(1, (4 * slots + tiles - 1) / tiles);
   int kc = kchunk_env > 0 ? kchunk_env : std::min(16, std::max(4, (g.nzl + want - 1) / want));
   kc = std::max(1, std::min(kc, g.nzl));
