@@ -1164,7 +1164,12 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
   a.nlist = lv.n;
   static const int fork_env = getenv("STK_LIST_FORK") ? atoi(getenv("STK_LIST_FORK")) : 1;
   const bool do_list = lv.n > 0;
-  const bool fork = do_list && fork_env && lv.side != nullptr;
+  // In-place velocity pass: the list rows (into cbuf) must read start-of-pass values; the
+  // face rows with truncated stencils (free slip, traction) couple to same-colour regular
+  // rows, which the stream kernel relaxes in place -- so the list kernel runs first, on
+  // the same stream (no overlap, deterministic).
+  const bool list_first = do_list && OP == OP_VEL && a.inplace && lv.S != nullptr;
+  const bool fork = do_list && !list_first && fork_env && lv.side != nullptr;
   if (fork) {
     if (cudaEventRecord(lv.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(lv.side, lv.ev_fork, 0) != cudaSuccess)
       return false;
@@ -1173,6 +1178,8 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
   static unsigned long long* tbuf = nullptr;
   if (trace && !tbuf) cudaMallocManaged(&tbuf, sizeof(unsigned long long) * 4096 * 10);
   a.trace = trace ? tbuf : nullptr;
+  if (list_first)
+    k_listx<FORM, OP><<<(unsigned)(((int64_t)lv.n * 16 + LX_NT - 1) / LX_NT), LX_NT, 0, st>>>(g, a, lv.S);
   k_stream<FORM, OP><<<dim3(grid), NT, sm, st>>>(mU, mP, g, a);
   if (trace) {  // debug: mean per-CTA cycle split of this launch
     cudaStreamSynchronize(st);
@@ -1184,7 +1191,7 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
             " | last warp: total %.0f wait %.0f sync %.0f (cycles)\n", FORM, OP, g.n, grid, kc, tot[0][4], tot[0][0],
             tot[0][1], tot[0][2], tot[0][3], tot[1][0], tot[1][1], tot[1][2]);
   }
-  if (do_list) {
+  if (do_list && !list_first) {
     if (lv.S) k_listx<FORM, OP><<<(unsigned)(((int64_t)lv.n * 16 + LX_NT - 1) / LX_NT), LX_NT, 0, fork ? lv.side : st>>>(g, a, lv.S);
     else k_list<FORM, OP><<<(lv.n + LIST_NT - 1) / LIST_NT, LIST_NT, 0, fork ? lv.side : st>>>(g, a);
   }
