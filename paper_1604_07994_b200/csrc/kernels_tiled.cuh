@@ -1168,7 +1168,10 @@ bool launch_stream_t(const DGrid& g, const double* inU, const double* inP, const
   // face rows with truncated stencils (free slip, traction) couple to same-colour regular
   // rows, which the stream kernel relaxes in place -- so the list kernel runs first, on
   // the same stream (no overlap, deterministic).
-  const bool list_first = do_list && OP == OP_VEL && a.inplace && lv.S != nullptr;
+  // (Dirichlet-only levels have no such rows -- Gamma_12 rows couple to other-colour or
+  // Gamma columns only -- and keep the overlapped fork.)
+  const bool face_rows = g.slipmask != 0u || (g.dirmask & 63u) != 63u;
+  const bool list_first = do_list && OP == OP_VEL && a.inplace && lv.S != nullptr && face_rows;
   const bool fork = do_list && !list_first && fork_env && lv.side != nullptr;
   if (fork) {
     if (cudaEventRecord(lv.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(lv.side, lv.ev_fork, 0) != cudaSuccess)
